@@ -1,0 +1,153 @@
+/*
+ * geninv.h -- C ABI of the B200-native (sm_100a) FP64 geninv library.
+ *
+ * Computes the Moore-Penrose inverse G+ of a real m x n matrix G with
+ * Courrieu's full-rank-Cholesky method (arXiv 0804.4809, "Fast Computation
+ * of Moore-Penrose Inverse Matrices"; PAPER.md line numbers cited as P:NN):
+ *
+ *   a0  if m < n: work with G G' (transpose branch), else G' G
+ *   a1  A = G'G (or GG'), s x s with s = min(m, n)
+ *   a2  tol = 1e-9 * min{A_ii : A_ii > 0}   (0 if none)
+ *   a3  rank-revealing full-rank Cholesky A = L L', natural column
+ *       order, a column is kept iff its pivot > tol (strict)        P:118-133, Eq.(1)
+ *   a4  B = L'L;  a5  M = inv(B) (SPD: Cholesky, triangular inverse,
+ *       product)
+ *   a6  K = L M, X = K K'  (= L M M L', Theorem 1)
+ *   a7  G+ = X G'  (m >= n)   or   G+ = G' X  (m < n)
+ *   a8  row-sharded Gram: A = sum_p G_p' G_p (caller all-reduces A)
+ *   a9  batched: many independent small G, one CTA per matrix
+ *
+ * Conventions (all entry points):
+ *   - FP64 (double), ROW-MAJOR storage: element (i, j) of a matrix with
+ *     leading dimension ld is at ptr[i * ld + j].
+ *   - Pointers named *_dev / G / Gp / A are DEVICE pointers on the handle's
+ *     device unless stated; *_host are host pointers (pinned memory gives
+ *     overlapped copies; pageable memory works but is slower).
+ *   - The caller owns G (never written), G+ and every output buffer; the
+ *     handle owns its workspace (about 7 s^2 doubles + split-K partials),
+ *     grown on demand and freed by geninv_destroy.  G and G+ must not alias.
+ *   - Work is enqueued on the handle's stream (geninv_set_stream).  Calls
+ *     that return a host-side rank / info synchronise that stream.
+ *   - Errors are status codes; nothing throws across the ABI.  A handle is
+ *     not thread-safe; separate handles are independent.
+ *   - Alignment: the TMA path needs 16-byte-aligned base pointers and even
+ *     leading dimensions; other inputs are rejected with GENINV_EALIGN.
+ */
+#ifndef GENINV_H_
+#define GENINV_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GENINV_API __attribute__((visibility("default")))
+#else
+#define GENINV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GENINV_OK = 0,
+  GENINV_EINVAL = 1,      /* bad size / leading dimension / null pointer */
+  GENINV_ENONFINITE = 2,  /* non-finite diagonal of A (NaN/Inf in G) */
+  GENINV_ENOTSPD = 3,     /* a5: a pivot <= 0 in the Cholesky of L'L (reading R8) */
+  GENINV_ECUDA = 4,       /* CUDA runtime / launch error */
+  GENINV_ENOMEM = 5,      /* device allocation failed */
+  GENINV_EALIGN = 6,      /* pointer not 16-byte aligned or odd leading dimension */
+  GENINV_ESTATE = 7       /* geninv_apply_d before geninv_from_gram_d, or shape mismatch */
+} geninv_status;
+
+/* Tolerance policy (SPEC ToleranceConfig).  NULL opts = the paper's policy. */
+typedef struct {
+  double tol_rel; /* relative factor, default 1e-9 */
+  double tol_abs; /* < 0: paper policy tol = tol_rel * min positive diag; >= 0: this absolute tol */
+} geninv_opts;
+
+/* Diagnostics of one factorisation (device values copied back to the host). */
+typedef struct {
+  double tol;        /* the tolerance actually used */
+  int64_t rank;      /* detected rank r */
+  int32_t transposed;/* 1 if the m < n branch was taken */
+  int32_t status;    /* geninv_status of the call */
+  double min_acc;    /* smallest accepted pivot c_k (before sqrt); +inf if none */
+  double max_drop;   /* largest |c_k| over dropped columns; 0 if none */
+  double min_pivot;  /* smallest c_k over all columns */
+} geninv_info;
+
+typedef struct geninv_handle_s *geninv_handle;
+
+/* Create a handle bound to CUDA device `device` with its own non-blocking stream. */
+GENINV_API geninv_status geninv_create(geninv_handle *h, int device);
+/* Use `stream` (a cudaStream_t passed as void*) for all later work; NULL = the legacy default
+ * stream.  Until this is called the handle uses its own non-blocking stream. */
+GENINV_API geninv_status geninv_set_stream(geninv_handle h, void *stream);
+GENINV_API geninv_status geninv_destroy(geninv_handle h);
+GENINV_API const char *geninv_strerror(geninv_status st);
+
+/* ---- whole path, single matrix (a0-a7) ------------------------------------
+ * G: m x n device, ld >= n.  Gp: n x m device, ldp >= m, overwritten.
+ * rank (host, may be NULL) receives r; info (host, may be NULL) diagnostics.
+ * Zero G -> rank 0 and G+ = 0 (reading R2).  Synchronises the stream. */
+GENINV_API geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp,
+                       int64_t ldp, int64_t *rank, const geninv_opts *opts, geninv_info *info);
+
+/* Same computation with HOST buffers G_host (m x n, ld) and Gp_host (n x m, ldp):
+ * the library stages G to the device in row chunks (copies overlapped with the
+ * Gram), and streams G+ back overlapped with the output product.  Device
+ * buffers for G and G+ chunks live in the handle's workspace. */
+GENINV_API geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, int64_t n, int64_t ld,
+                            double *Gp_host, int64_t ldp, int64_t *rank, const geninv_opts *opts,
+                            geninv_info *info);
+
+/* ---- batched small matrices (a9) ------------------------------------------
+ * `batch` independent m x n matrices: matrix b at G + b*strideG (device, ld >= n),
+ * G+ of matrix b written at Gp + b*strideGp (n x m, ldp >= m).  rank_dev:
+ * device int32[batch].  Requires min(m, n) <= 64 and max(m, n) <= 128.
+ * Does not synchronise. */
+GENINV_API geninv_status geninv_batched_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int64_t strideG,
+                               int64_t batch, double *Gp, int64_t ldp, int64_t strideGp, int32_t *rank_dev,
+                               const geninv_opts *opts);
+
+/* ---- split form (row sharding, a8) -----------------------------------------
+ * geninv_gram_d: A (s x s, lda >= s, device, caller-owned) = G'G if trans == 0
+ *   (s = n), G G' if trans == 1 (s = m).  Lower triangle (and diagonal) written.
+ *   For row shards with trans == 0 the caller sums A over ranks (all-reduce)
+ *   before geninv_from_gram_d.  Does not synchronise.
+ * geninv_from_gram_d: steps a2-a6 on the (summed) A: tol, full-rank Cholesky,
+ *   M = inv(L'L), X = (LM)(LM)' kept in the handle.  Synchronises; rank/info out.
+ * geninv_apply_d: step a7 with the handle's X: trans == 0: Gp (n x m_local) =
+ *   X G_local'  (a column block of G+ for a row shard); trans == 1: Gp = G' X.
+ *   Does not synchronise. */
+GENINV_API geninv_status geninv_gram_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int32_t trans,
+                            double *A, int64_t lda);
+GENINV_API geninv_status geninv_from_gram_d(geninv_handle h, const double *A, int64_t s, int64_t lda, int64_t *rank,
+                                 const geninv_opts *opts, geninv_info *info);
+GENINV_API geninv_status geninv_apply_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int32_t trans,
+                             double *Gp, int64_t ldp);
+
+/* ---- single steps, exposed for step-level parity tests ----------------------
+ * geninv_frchol_d (a2+a3): on A (s x s lower, lda): tol per opts, then the
+ *   full-rank Cholesky.  L (s x s, ldl, device) receives the s x r factor in
+ *   its first r columns (zeros above pivots and in columns >= r); piv_dev
+ *   (device int32[s]) the pivot row of each kept column.  Synchronises.
+ * geninv_spd_inverse_d (a5): M (r x r, ldm) = inv(B) for SPD B (r x r lower,
+ *   ldb) via Cholesky, triangular inverse and C^-T C^-1; GENINV_ENOTSPD on a
+ *   pivot <= 0.  Synchronises.
+ * geninv_copy_x: copies the handle's X = L M M L' (s x s, from the last
+ *   geninv_d / geninv_from_gram_d) into the device buffer X (ldx >= s) and
+ *   synchronises; X == NULL only reports s.  GENINV_ESTATE before any call. */
+GENINV_API geninv_status geninv_frchol_d(geninv_handle h, const double *A, int64_t s, int64_t lda, double *L, int64_t ldl,
+                              int32_t *piv_dev, int64_t *rank, const geninv_opts *opts, geninv_info *info);
+GENINV_API geninv_status geninv_spd_inverse_d(geninv_handle h, const double *B, int64_t r, int64_t ldb, double *M,
+                                   int64_t ldm);
+GENINV_API geninv_status geninv_copy_x(geninv_handle h, double *X, int64_t ldx, int64_t *s);
+
+/* Number of kernels this handle has launched so far (launch accounting for bench.py). */
+GENINV_API int64_t geninv_launch_count(geninv_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GENINV_H_ */

@@ -1,0 +1,42 @@
+// Host-side description of one FP64 tensor-core GEMM launch (see gemm.cuh).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gi {
+
+struct Mat {               // row-major device matrix (or batch of equally-shaped blocks)
+  const double *ptr = nullptr;
+  long long ld = 0, rows = 0, cols = 0;
+  int batch = 1;
+  long long bstride = 0;   // elements between batch items
+};
+
+enum Tile { TILE_128x128 = 0, TILE_128x32 = 1 };
+
+struct GemmOp {
+  Mat A;  bool a_kmajor = true;  int a_mn0 = 0, a_k0 = 0;
+  Mat B;  bool b_kmajor = true;  int b_mn0 = 0, b_k0 = 0;
+  double *C = nullptr; long long ldc = 0, c_bstride = 0;
+  const double *C0 = nullptr; long long ldc0 = 0, c0_bstride = 0;
+  double alpha = 1.0;
+  int M = 0, N = 0, K = 0;
+  const int *K_dev = nullptr;   // device-side K (overrides K; K is then the upper bound)
+  int batch = 1;
+  bool lower = false, mirror = false;
+  int splits = 1; long long split_stride = 0;
+  Tile tile = TILE_128x128;
+};
+
+// Enqueue one GEMM on `st`.  Returns cudaSuccess or the launch / encode error.
+cudaError_t gemm(const GemmOp &op, cudaStream_t st);
+
+// Sum split-K partial slices in a fixed order:  out = C0 + alpha * sum_z P[z]
+// (C0 may be null).  lower: only elements with j <= i (square M == N).
+cudaError_t splitk_reduce(const double *P, long long split_stride, int splits, long long ldp, double *out,
+                          long long ldo, const double *C0, long long ldc0, double alpha, int M, int N, bool lower,
+                          cudaStream_t st);
+
+int num_sms();
+
+}  // namespace gi

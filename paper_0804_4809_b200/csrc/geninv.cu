@@ -1,0 +1,603 @@
+// Host orchestrator + C ABI (include/geninv.h) of the sm_100a geninv library.
+//
+// Plans the step sequence of PAPER.md P:105-140 for (m, n), owns the
+// workspace and the stream, and enqueues the kernels:
+//   a1 gram (gemm.cu, lower tiles, split-K + fixed-order reduction)
+//   a2 tolerance, a3 frchol (frchol.cu)         -- one host sync to read r
+//   a4 B = L'L, a5 POTRF (frchol mode 1) + TRTRI (spdinv.cu) + C^-T C^-1
+//   a6 K = L M, X = K K'  (flop-minimal reassociation of P:137/P:139, R9)
+//   a7 G+ = X G' or G' X
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "../../include/geninv.h"
+#include "gemm_host.h"
+#include "kernels.h"
+
+using namespace gi;
+
+struct geninv_handle_s {
+  int device = 0;
+  cudaStream_t own = nullptr, st = nullptr, st2 = nullptr;
+  cudaEvent_t ev[4] = {};
+  // s x s workspaces (leading dimension ld >= round_up(s, 32))
+  int s_cap = 0;
+  long long ld = 0;
+  double *A = nullptr, *L = nullptr, *Bm = nullptr, *Cf = nullptr, *Ci = nullptr, *Mm = nullptr, *Kb = nullptr,
+         *X = nullptr, *T = nullptr;
+  double *Wp = nullptr;
+  long long wp_elems = 0;
+  double *part = nullptr;  // Gram split-K partials
+  size_t part_bytes = 0;
+  int *rk = nullptr, *piv = nullptr, *rk2 = nullptr, *piv2 = nullptr;
+  FactorStats *fs = nullptr, *fs2 = nullptr;
+  // host-buffer path staging
+  double *Gdev = nullptr, *Gpchunk[2] = {nullptr, nullptr};
+  size_t gdev_bytes = 0, chunk_bytes = 0;
+  // state of the last factorisation (for geninv_apply_d)
+  int x_s = -1;
+  int last_rank = 0;
+  long long launches = 0;
+};
+
+namespace {
+
+geninv_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return GENINV_OK;
+  if (e == cudaErrorMemoryAllocation) return GENINV_ENOMEM;
+  if (e == cudaErrorMisalignedAddress) return GENINV_EALIGN;
+  fprintf(stderr, "[geninv] CUDA error: %s\n", cudaGetErrorString(e));
+  return GENINV_ECUDA;
+}
+
+#define GI_TRY(expr)                                  \
+  do {                                                \
+    cudaError_t _e = (expr);                          \
+    if (_e != cudaSuccess) return cuda_status(_e);    \
+  } while (0)
+
+#define GI_TRYS(expr)                                 \
+  do {                                                \
+    geninv_status _s = (expr);                        \
+    if (_s != GENINV_OK) return _s;                   \
+  } while (0)
+
+void free_ws(geninv_handle h) {
+  double **bufs[] = {&h->A, &h->L, &h->Bm, &h->Cf, &h->Ci, &h->Mm, &h->Kb, &h->X, &h->T, &h->Wp};
+  for (auto b : bufs) {
+    if (*b) cudaFree(*b);
+    *b = nullptr;
+  }
+  int **ibufs[] = {&h->rk, &h->piv, &h->rk2, &h->piv2};
+  for (auto b : ibufs) {
+    if (*b) cudaFree(*b);
+    *b = nullptr;
+  }
+  if (h->fs) cudaFree(h->fs);
+  if (h->fs2) cudaFree(h->fs2);
+  h->fs = h->fs2 = nullptr;
+  h->s_cap = 0;
+  h->x_s = -1;
+}
+
+geninv_status ensure_ws(geninv_handle h, int s) {
+  if (s <= h->s_cap) return GENINV_OK;
+  cudaStreamSynchronize(h->st);
+  free_ws(h);
+  const long long ld = (s + 31) / 32 * 32;
+  const size_t sq = (size_t)ld * ld * sizeof(double);
+  double **bufs[] = {&h->A, &h->L, &h->Bm, &h->Cf, &h->Ci, &h->Mm, &h->Kb, &h->X, &h->T};
+  for (auto b : bufs) GI_TRY(cudaMalloc(b, sq));
+  h->wp_elems = 16LL * ld * PB;
+  GI_TRY(cudaMalloc(&h->Wp, h->wp_elems * sizeof(double)));
+  const int np = (int)(ld / PB) + 2;
+  GI_TRY(cudaMalloc(&h->rk, np * sizeof(int)));
+  GI_TRY(cudaMalloc(&h->rk2, np * sizeof(int)));
+  GI_TRY(cudaMalloc(&h->piv, ld * sizeof(int)));
+  GI_TRY(cudaMalloc(&h->piv2, ld * sizeof(int)));
+  GI_TRY(cudaMalloc(&h->fs, sizeof(FactorStats)));
+  GI_TRY(cudaMalloc(&h->fs2, sizeof(FactorStats)));
+  h->s_cap = (int)ld;
+  h->ld = ld;
+  return GENINV_OK;
+}
+
+geninv_status ensure_part(geninv_handle h, size_t bytes) {
+  if (bytes <= h->part_bytes) return GENINV_OK;
+  cudaStreamSynchronize(h->st);
+  if (h->part) cudaFree(h->part);
+  h->part = nullptr;
+  h->part_bytes = 0;
+  GI_TRY(cudaMalloc(&h->part, bytes));
+  h->part_bytes = bytes;
+  return GENINV_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Split-K count for `tiles` output tiles over `nslab` k-slabs: the smallest
+// split whose wave efficiency (1 CTA / SM) is within 2 % of the best.
+int pick_splits(long long tiles, long long nslab) {
+  const int sms = num_sms();
+  double eff[17];
+  double best = 0;
+  for (int S = 1; S <= 16; ++S) {
+    eff[S] = 0;
+    if (S > 1 && nslab / S < 16) break;
+    const long long work = tiles * S;
+    const long long waves = (work + sms - 1) / sms;
+    eff[S] = (double)work / (double)(waves * sms);
+    best = std::max(best, eff[S]);
+  }
+  for (int S = 1; S <= 16; ++S)
+    if (eff[S] >= best - 0.02) return S;
+  return 1;
+}
+
+// a1: A (s x s, lower) = G'G (trans == 0) or GG' (trans == 1).
+geninv_status gram(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *A,
+                   long long lda, const double *accumulate = nullptr) {
+  const long long s = trans ? m : n, ell = trans ? n : m;
+  GemmOp op;
+  op.A = Mat{G, ld, m, n};
+  op.B = op.A;
+  op.a_kmajor = op.b_kmajor = (trans != 0);  // T: A[i][j] = sum_k G[i][k] G[j][k]; N: sum_k G[k][i] G[k][j]
+  op.M = op.N = (int)s;
+  op.K = (int)ell;
+  op.lower = true;
+  const long long mt = (s + 127) / 128;
+  const long long tiles = mt * (mt + 1) / 2;
+  const int S = pick_splits(tiles, (ell + 15) / 16);
+  if (S == 1 && !accumulate) {
+    op.C = A;
+    op.ldc = lda;
+    GI_TRY(gemm(op, h->st));
+    h->launches += 1;
+    return GENINV_OK;
+  }
+  const long long pstride = (long long)h->ld * h->ld;
+  GI_TRYS(ensure_part(h, (size_t)S * pstride * sizeof(double)));
+  op.C = h->part;
+  op.ldc = h->ld;
+  op.splits = S;
+  op.split_stride = pstride;
+  GI_TRY(gemm(op, h->st));
+  GI_TRY(splitk_reduce(h->part, pstride, S, h->ld, A, lda, accumulate, lda, 1.0, (int)s, (int)s, true, h->st));
+  h->launches += 2;
+  return GENINV_OK;
+}
+
+double tol_rel_of(const geninv_opts *o) { return o ? o->tol_rel : 1e-9; }
+double tol_abs_of(const geninv_opts *o) { return o ? o->tol_abs : -1.0; }
+
+// a2 + a3 on h->A-like input; L zeroed here.  Returns rank via host sync.
+geninv_status factor(geninv_handle h, const double *A, long long lda, int s, double *L, long long ldl, int *piv,
+                     const geninv_opts *opts, int *rank_out, FactorStats *hst) {
+  GI_TRY(tolerance(A, lda, s, tol_rel_of(opts), tol_abs_of(opts), h->fs, h->st));
+  GI_TRY(cudaMemsetAsync(L, 0, (size_t)s * ldl * sizeof(double), h->st));
+  GI_TRY(frchol(A, lda, s, L, ldl, piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, h->st));
+  const int np = (s + PB - 1) / PB;
+  h->launches += 1 + np + (np - 1);
+  int r = 0;
+  GI_TRY(cudaMemcpyAsync(&r, h->rk + np, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  GI_TRY(cudaMemcpyAsync(hst, h->fs, sizeof(FactorStats), cudaMemcpyDeviceToHost, h->st));
+  GI_TRY(cudaStreamSynchronize(h->st));
+  *rank_out = r;
+  if (hst->flags & 1) return GENINV_ENONFINITE;
+  return GENINV_OK;
+}
+
+// a5: M (r x r, ldm, full symmetric) = inv(B), B SPD (lower, ldb).  No sync.
+geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb, double *M, long long ldm) {
+  const long long ld = h->ld;
+  const int r_pad = (r + 31) / 32 * 32;
+  GI_TRY(cudaMemsetAsync(h->Cf, 0, (size_t)r_pad * ld * sizeof(double), h->st));
+  GI_TRY(cudaMemsetAsync(h->Ci, 0, (size_t)r_pad * ld * sizeof(double), h->st));
+  GI_TRY(tolerance(B, ldb, r, 0.0, 0.0, h->fs2, h->st));
+  GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st));
+  GI_TRY(trtri_lower(h->Cf, ld, r, h->Ci, ld, h->T, h->st));
+  // M = C^-T C^-1 : M[i][j] = sum_k Ci[k][i] Ci[k][j]
+  GemmOp op;
+  op.A = Mat{h->Ci, ld, r_pad, r_pad};
+  op.B = op.A;
+  op.a_kmajor = op.b_kmajor = false;
+  op.M = op.N = r;
+  op.K = r_pad;
+  op.lower = true;
+  op.mirror = true;
+  op.C = M;
+  op.ldc = ldm;
+  GI_TRY(gemm(op, h->st));
+  const int np = (r + PB - 1) / PB;
+  int lev = 0;
+  for (int hh = 32; hh < r_pad; hh *= 2) ++lev;
+  h->launches += 1 + np + (np - 1) + 2 + 4 * lev + 1;
+  return GENINV_OK;
+}
+
+// a4-a6 after the factorisation: X (s x s, full) = L M M L'.
+geninv_status build_x(geninv_handle h, int s, int r) {
+  const long long ld = h->ld;
+  if (r == 0) {
+    GI_TRY(cudaMemsetAsync(h->X, 0, (size_t)s * ld * sizeof(double), h->st));
+    return GENINV_OK;
+  }
+  // a4: B = L'L (r x r, lower): B[i][j] = sum_k L[k][i] L[k][j]
+  GemmOp b;
+  b.A = Mat{h->L, ld, s, ld};
+  b.B = b.A;
+  b.a_kmajor = b.b_kmajor = false;
+  b.M = b.N = r;
+  b.K = s;
+  b.lower = true;
+  b.C = h->Bm;
+  b.ldc = ld;
+  GI_TRY(gemm(b, h->st));
+  h->launches += 1;
+  // a5
+  GI_TRYS(spd_inverse(h, h->Bm, r, ld, h->Mm, ld));
+  // a6: K = L M (s x r):  K[i][c] = sum_j L[i][j] M[j][c]
+  GemmOp k;
+  k.A = Mat{h->L, ld, s, r};
+  k.a_kmajor = true;
+  k.B = Mat{h->Mm, ld, r, r};
+  k.b_kmajor = false;
+  k.M = s;
+  k.N = r;
+  k.K = r;
+  k.C = h->Kb;
+  k.ldc = ld;
+  GI_TRY(gemm(k, h->st));
+  // X = K K' (s x s, full symmetric)
+  GemmOp x;
+  x.A = Mat{h->Kb, ld, s, r};
+  x.B = x.A;
+  x.a_kmajor = x.b_kmajor = true;
+  x.M = x.N = s;
+  x.K = r;
+  x.lower = true;
+  x.mirror = true;
+  x.C = h->X;
+  x.ldc = ld;
+  GI_TRY(gemm(x, h->st));
+  h->launches += 2;
+  return GENINV_OK;
+}
+
+// a7: Gp = X G' (trans 0: Gp is n x m) or G' X (trans 1: Gp is n x m).
+geninv_status apply(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *Gp,
+                    long long ldp, cudaStream_t st) {
+  const long long s = trans ? m : n;
+  GemmOp op;
+  if (!trans) {
+    // Gp[i][j] = sum_k X[i][k] G[j][k],  i < n = s, j < m
+    op.A = Mat{h->X, h->ld, s, s};
+    op.a_kmajor = true;
+    op.B = Mat{G, ld, m, n};
+    op.b_kmajor = true;
+    op.M = (int)s;
+    op.N = (int)m;
+  } else {
+    // Gp[i][j] = sum_k G[k][i] X[k][j] = sum_k G[k][i] X[j][k],  i < n, j < m = s
+    op.A = Mat{G, ld, m, n};
+    op.a_kmajor = false;
+    op.B = Mat{h->X, h->ld, s, s};
+    op.b_kmajor = true;
+    op.M = (int)n;
+    op.N = (int)s;
+  }
+  op.K = (int)s;
+  op.C = Gp;
+  op.ldc = ldp;
+  GI_TRY(gemm(op, st));
+  h->launches += 1;
+  return GENINV_OK;
+}
+
+void fill_info(geninv_info *info, const FactorStats &fs, int r, int tr, geninv_status st) {
+  if (!info) return;
+  info->tol = fs.tol;
+  info->rank = r;
+  info->transposed = tr;
+  info->status = st;
+  info->min_acc = fs.min_acc;
+  info->max_drop = fs.max_drop;
+  info->min_pivot = fs.min_pivot;
+}
+
+geninv_status check_g(const double *G, long long m, long long n, long long ld) {
+  if (!G || m < 1 || n < 1 || ld < n) return GENINV_EINVAL;
+  if (m > 0x7fffffffLL || n > 0x7fffffffLL) return GENINV_EINVAL;
+  if (!aligned16(G) || (ld & 1)) return GENINV_EALIGN;
+  return GENINV_OK;
+}
+
+// Steps a2-a6 on A (s x s lower, lda); leaves X in the handle.
+geninv_status from_gram(geninv_handle h, const double *A, int s, long long lda, const geninv_opts *opts, int *r_out,
+                        FactorStats *fs) {
+  GI_TRYS(ensure_ws(h, s));
+  int r = 0;
+  geninv_status st = factor(h, A, lda, s, h->L, h->ld, h->piv, opts, &r, fs);
+  if (st != GENINV_OK) return st;
+  GI_TRYS(build_x(h, s, r));
+  h->x_s = s;
+  h->last_rank = r;
+  *r_out = r;
+  return GENINV_OK;
+}
+
+geninv_status finish_spd_check(geninv_handle h, int r) {
+  if (r == 0) return GENINV_OK;
+  int flags = 0;
+  GI_TRY(cudaMemcpyAsync(&flags, &h->fs2->flags, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  GI_TRY(cudaStreamSynchronize(h->st));
+  return (flags & 2) ? GENINV_ENOTSPD : GENINV_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+geninv_status geninv_create(geninv_handle *out, int device) {
+  if (!out) return GENINV_EINVAL;
+  auto *h = new geninv_handle_s();
+  h->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_status(e);
+  }
+  h->st = h->own;
+  *out = h;
+  return GENINV_OK;
+}
+
+geninv_status geninv_set_stream(geninv_handle h, void *stream) {
+  if (!h) return GENINV_EINVAL;
+  h->st = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
+  return GENINV_OK;
+}
+
+geninv_status geninv_destroy(geninv_handle h) {
+  if (!h) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->st);
+  free_ws(h);
+  if (h->part) cudaFree(h->part);
+  if (h->Gdev) cudaFree(h->Gdev);
+  for (auto &c : h->Gpchunk)
+    if (c) cudaFree(c);
+  for (auto &ev : h->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->st2) cudaStreamDestroy(h->st2);
+  if (h->own) cudaStreamDestroy(h->own);
+  delete h;
+  return GENINV_OK;
+}
+
+const char *geninv_strerror(geninv_status st) {
+  switch (st) {
+    case GENINV_OK: return "ok";
+    case GENINV_EINVAL: return "invalid argument";
+    case GENINV_ENONFINITE: return "non-finite entry in G (non-finite Gram diagonal)";
+    case GENINV_ENOTSPD: return "L'L is not numerically SPD (pivot <= 0 in its Cholesky)";
+    case GENINV_ECUDA: return "CUDA error";
+    case GENINV_ENOMEM: return "device out of memory";
+    case GENINV_EALIGN: return "pointer not 16-byte aligned or odd leading dimension";
+    case GENINV_ESTATE: return "no factorisation of matching size in the handle";
+  }
+  return "unknown status";
+}
+
+geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp, int64_t ldp,
+                       int64_t *rank, const geninv_opts *opts, geninv_info *info) {
+  if (!h || !Gp || ldp < m) return GENINV_EINVAL;
+  GI_TRYS(check_g(G, m, n, ld));
+  cudaSetDevice(h->device);
+  const int tr = m < n;  // P:109 (strict; m == n takes the N branch, R6)
+  const int s = (int)(tr ? m : n);
+  GI_TRYS(ensure_ws(h, s));
+  GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
+  int r = 0;
+  FactorStats fs{};
+  geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs);
+  if (st == GENINV_OK) st = apply(h, G, m, n, ld, tr, Gp, ldp, h->st);
+  if (st == GENINV_OK) st = finish_spd_check(h, r);
+  if (st == GENINV_OK) {
+    cudaError_t e = cudaStreamSynchronize(h->st);
+    if (e != cudaSuccess) st = cuda_status(e);
+  }
+  if (rank) *rank = r;
+  fill_info(info, fs, r, tr, st);
+  return st;
+}
+
+geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, int64_t n, int64_t ld, double *Gp_host,
+                            int64_t ldp, int64_t *rank, const geninv_opts *opts, geninv_info *info) {
+  if (!h || !G_host || !Gp_host || m < 1 || n < 1 || ld < n || ldp < m) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  const int tr = m < n;
+  const int s = (int)(tr ? m : n);
+  const long long ldg = (n + 1) / 2 * 2;  // device copy: even leading dimension
+  const size_t gbytes = (size_t)m * ldg * sizeof(double);
+  if (gbytes > h->gdev_bytes) {
+    if (h->Gdev) cudaFree(h->Gdev);
+    h->Gdev = nullptr;
+    h->gdev_bytes = 0;
+    GI_TRY(cudaMalloc(&h->Gdev, gbytes));
+    h->gdev_bytes = gbytes;
+  }
+  GI_TRYS(ensure_ws(h, s));
+  // ---- H2D in row chunks, the Gram of each chunk accumulated as soon as it lands
+  //      (N branch: A = sum_c G_c' G_c; T branch: the Gram needs all columns -> one pass after the copy)
+  const long long rows_per = tr ? m : std::max<long long>(1, (256LL << 20) / (ldg * 8));
+  int nch = 0;
+  for (long long r0 = 0; r0 < m; r0 += rows_per, ++nch) {
+    const long long rows = std::min(rows_per, m - r0);
+    GI_TRY(cudaMemcpy2DAsync(h->Gdev + r0 * ldg, ldg * 8, G_host + r0 * ld, ld * 8, n * 8, rows,
+                             cudaMemcpyHostToDevice, h->st2));
+    GI_TRY(cudaEventRecord(h->ev[0], h->st2));
+    GI_TRY(cudaStreamWaitEvent(h->st, h->ev[0], 0));
+    if (!tr)
+      GI_TRYS(gram(h, h->Gdev + r0 * ldg, rows, n, ldg, 0, h->A, h->ld, r0 == 0 ? nullptr : h->A));
+  }
+  if (tr) GI_TRYS(gram(h, h->Gdev, m, n, ldg, 1, h->A, h->ld));
+  int r = 0;
+  FactorStats fs{};
+  geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs);
+  if (st == GENINV_OK) st = finish_spd_check(h, r);
+  if (st != GENINV_OK) {
+    fill_info(info, fs, r, tr, st);
+    return st;
+  }
+  // ---- output in chunks, D2H of chunk c overlapped with the product of chunk c + 1
+  //      N: column block j0..j1 of G+ (n x m) = X G[j0:j1]';  T: row block of G+ = G[:, i0:i1]' X
+  const long long cw = tr ? std::max<long long>(1, (256LL << 20) / (m * 8)) : rows_per;
+  const long long total = tr ? n : m;
+  const size_t cbytes = (size_t)cw * s * sizeof(double) + 256;
+  if (cbytes > h->chunk_bytes) {
+    for (auto &c : h->Gpchunk) {
+      if (c) cudaFree(c);
+      c = nullptr;
+    }
+    h->chunk_bytes = 0;
+    for (auto &c : h->Gpchunk) GI_TRY(cudaMalloc(&c, cbytes));
+    h->chunk_bytes = cbytes;
+  }
+  int buf = 0;
+  bool pending[2] = {false, false};
+  for (long long c0 = 0; c0 < total; c0 += cw, buf ^= 1) {
+    const long long w = std::min(cw, total - c0);
+    if (pending[buf]) GI_TRY(cudaStreamWaitEvent(h->st, h->ev[2 + buf], 0));  // chunk buffer free again
+    double *dst = h->Gpchunk[buf];
+    if (!tr) {
+      // chunk (s x w, ld wpad) = X G[c0:c0+w]'
+      const long long wpad = (w + 1) / 2 * 2;
+      GI_TRYS(apply(h, h->Gdev + c0 * ldg, w, n, ldg, 0, dst, wpad, h->st));
+      GI_TRY(cudaEventRecord(h->ev[0], h->st));
+      GI_TRY(cudaStreamWaitEvent(h->st2, h->ev[0], 0));
+      GI_TRY(cudaMemcpy2DAsync(Gp_host + c0, ldp * 8, dst, wpad * 8, w * 8, s, cudaMemcpyDeviceToHost, h->st2));
+    } else {
+      // chunk (w x s, ld s) = G[:, c0:c0+w]' X : A-op is the column block of G (m x w)
+      GemmOp op;
+      op.A = Mat{h->Gdev, ldg, m, n};
+      op.a_kmajor = false;
+      op.a_mn0 = (int)c0;
+      op.B = Mat{h->X, h->ld, s, s};
+      op.b_kmajor = true;
+      op.M = (int)w;
+      op.N = s;
+      op.K = s;
+      op.C = dst;
+      op.ldc = s;
+      GI_TRY(gemm(op, h->st));
+      h->launches += 1;
+      GI_TRY(cudaEventRecord(h->ev[0], h->st));
+      GI_TRY(cudaStreamWaitEvent(h->st2, h->ev[0], 0));
+      GI_TRY(cudaMemcpy2DAsync(Gp_host + c0 * ldp, ldp * 8, dst, (size_t)s * 8, (size_t)s * 8, w,
+                               cudaMemcpyDeviceToHost, h->st2));
+    }
+    GI_TRY(cudaEventRecord(h->ev[2 + buf], h->st2));
+    pending[buf] = true;
+  }
+  GI_TRY(cudaStreamSynchronize(h->st2));
+  GI_TRY(cudaStreamSynchronize(h->st));
+  if (rank) *rank = r;
+  fill_info(info, fs, r, tr, GENINV_OK);
+  return GENINV_OK;
+}
+
+geninv_status geninv_batched_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int64_t strideG,
+                               int64_t batch, double *Gp, int64_t ldp, int64_t strideGp, int32_t *rank_dev,
+                               const geninv_opts *opts) {
+  if (!h || batch < 0 || m < 1 || n < 1 || ld < n || ldp < m) return GENINV_EINVAL;
+  if (batch == 0) return GENINV_OK;
+  if (!G || !Gp || !rank_dev) return GENINV_EINVAL;
+  if (std::min(m, n) > 64 || std::max(m, n) > 128) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  GI_TRY(batched_geninv(G, (int)m, (int)n, ld, strideG, batch, Gp, ldp, strideGp, rank_dev, tol_rel_of(opts),
+                        tol_abs_of(opts), h->st));
+  h->launches += 1;
+  return GENINV_OK;
+}
+
+geninv_status geninv_gram_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int32_t trans,
+                            double *A, int64_t lda) {
+  if (!h || !A) return GENINV_EINVAL;
+  GI_TRYS(check_g(G, m, n, ld));
+  const long long s = trans ? m : n;
+  if (lda < s) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  GI_TRYS(ensure_ws(h, (int)s));
+  return gram(h, G, m, n, ld, trans ? 1 : 0, A, lda);
+}
+
+geninv_status geninv_from_gram_d(geninv_handle h, const double *A, int64_t s, int64_t lda, int64_t *rank,
+                                 const geninv_opts *opts, geninv_info *info) {
+  if (!h || !A || s < 1 || lda < s) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  int r = 0;
+  FactorStats fs{};
+  geninv_status st = from_gram(h, A, (int)s, lda, opts, &r, &fs);
+  if (st == GENINV_OK) st = finish_spd_check(h, r);
+  if (rank) *rank = r;
+  fill_info(info, fs, r, 0, st);
+  return st;
+}
+
+geninv_status geninv_apply_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int32_t trans,
+                             double *Gp, int64_t ldp) {
+  if (!h || !Gp) return GENINV_EINVAL;
+  GI_TRYS(check_g(G, m, n, ld));
+  const long long s = trans ? m : n;
+  if (h->x_s != s) return GENINV_ESTATE;
+  if (ldp < (trans ? s : m)) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  return apply(h, G, m, n, ld, trans ? 1 : 0, Gp, ldp, h->st);
+}
+
+geninv_status geninv_frchol_d(geninv_handle h, const double *A, int64_t s, int64_t lda, double *L, int64_t ldl,
+                              int32_t *piv_dev, int64_t *rank, const geninv_opts *opts, geninv_info *info) {
+  if (!h || !A || !L || !piv_dev || s < 1 || lda < s || ldl < s) return GENINV_EINVAL;
+  if (!aligned16(L) || (ldl & 1)) return GENINV_EALIGN;
+  cudaSetDevice(h->device);
+  GI_TRYS(ensure_ws(h, (int)s));
+  int r = 0;
+  FactorStats fs{};
+  geninv_status st = factor(h, A, lda, (int)s, L, ldl, piv_dev, opts, &r, &fs);
+  if (rank) *rank = r;
+  fill_info(info, fs, r, 0, st);
+  return st;
+}
+
+geninv_status geninv_spd_inverse_d(geninv_handle h, const double *B, int64_t r, int64_t ldb, double *M, int64_t ldm) {
+  if (!h || !B || !M || r < 1 || ldb < r || ldm < r) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  GI_TRYS(ensure_ws(h, (int)r));
+  GI_TRYS(spd_inverse(h, B, (int)r, ldb, M, ldm));
+  return finish_spd_check(h, (int)r);
+}
+
+geninv_status geninv_copy_x(geninv_handle h, double *X, int64_t ldx, int64_t *s) {
+  if (!h) return GENINV_EINVAL;
+  if (h->x_s < 0) return GENINV_ESTATE;
+  if (s) *s = h->x_s;
+  if (!X) return GENINV_OK;
+  if (ldx < h->x_s) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  GI_TRY(cudaMemcpy2DAsync(X, ldx * 8, h->X, h->ld * 8, (size_t)h->x_s * 8, h->x_s, cudaMemcpyDeviceToDevice, h->st));
+  GI_TRY(cudaStreamSynchronize(h->st));
+  return GENINV_OK;
+}
+
+int64_t geninv_launch_count(geninv_handle h) { return h ? h->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+// Host entry points of the geninv step kernels (frchol.cu, spdinv.cu, batched.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace gi {
+
+constexpr int PB = 32;  // panel width of the blocked full-rank Cholesky
+
+// Device-side diagnostics of one factorisation run.
+struct FactorStats {
+  double min_acc;    // min accepted pivot
+  double max_drop;   // max |dropped pivot|
+  double min_pivot;  // min pivot
+  double tol;        // tolerance used
+  int flags;         // bit0: non-finite diagonal, bit1: non-SPD pivot (mode 1)
+  int pad;
+};
+
+// a2: tol = tol_abs >= 0 ? tol_abs : tol_rel * min{A_ii > 0} (0 if none); also
+// initialises the stats block and flags a non-finite diagonal.
+cudaError_t tolerance(const double *A, long long lda, int s, double tol_rel, double tol_abs, FactorStats *st,
+                      cudaStream_t stream);
+
+// a3: blocked left-looking rank-revealing Cholesky.  L (s x s, ldl) must be
+// zero on entry; rk: device int[ceil(s/PB)+1] (rk[p] = rank before panel p,
+// rk[npanels] = final rank); piv: device int[s]; Wp: split-K workspace of
+// wp_elems doubles (>= 16 * s * PB).  mode 0: drop iff pivot <= tol (paper);
+// mode 1: SPD (accept iff pivot > 0, flag bit1 otherwise).
+cudaError_t frchol(const double *A, long long lda, int s, double *L, long long ldl, int *piv, int *rk,
+                   FactorStats *st, int mode, double *Wp, long long wp_elems, cudaStream_t stream);
+
+// a5 pieces: Cinv = C^-1 for lower-triangular C (r x r, ldc) padded to
+// r_pad = round_up(r, 32) with an identity block; C and Cinv are r_pad x r_pad
+// buffers (ld), C zero outside its r x r lower triangle, Cinv zero on entry.
+// T: workspace of r_pad * r_pad doubles.
+cudaError_t trtri_lower(double *C, long long ldc, int r, double *Cinv, long long ldi, double *T,
+                        cudaStream_t stream);
+
+// a9: batched small geninv, one CTA per matrix.
+cudaError_t batched_geninv(const double *G, int m, int n, long long ld, long long strideG, long long batch,
+                           double *Gp, long long ldp, long long strideGp, int *rank, double tol_rel,
+                           double tol_abs, cudaStream_t stream);
+
+}  // namespace gi

@@ -1,0 +1,221 @@
+"""End-to-end parity of the CUDA path (through the C ABI) against the oracle (`-m gpu`).
+
+Gates (north star), for inputs whose decision margins are far
+from the tolerance (predicate Q, computed from the ORACLE's run):
+  rank bit-exact;  ||G+_gpu - G+_oracle||_F / ||G+_oracle||_F <= 1e-9;
+  each relative Penrose residual <= 1e-10 (C5: <= 1e-10 on Q*, <= 1e-9 on Q).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import checks as C
+from oracle import geninv_oracle as O
+from paper_0804_4809_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+
+REL = 1e-9
+PENROSE = 1e-10
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_0804_4809_b200.binding import Handle
+    return Handle(0)
+
+
+def to_dev(G):
+    m, n = G.shape
+    ld = (n + 1) // 2 * 2
+    t = torch.zeros(m, ld, dtype=torch.float64, device="cuda")
+    t[:, :n] = torch.as_tensor(G)
+    return t[:, :n]
+
+
+def run(H, G, **kw):
+    Gp, info = H.geninv_d(to_dev(G), **kw)
+    return Gp.cpu().numpy(), info
+
+
+def penrose_gpu(G, X):
+    """Relative Penrose residuals with fresh cuBLAS products (test-only checker)."""
+    G = torch.as_tensor(G).cuda()
+    X = torch.as_tensor(X).cuda()
+    GX, XG = G @ X, X @ G
+    E = [GX @ G - G, XG @ X - X, GX.T - GX, XG.T - XG]
+    D = [G, X, GX, XG]
+    return [float(torch.linalg.norm(e) / torch.linalg.norm(d)) for e, d in zip(E, D)]
+
+
+@pytest.mark.parametrize("ex", GOLD["geninv"], ids=lambda e: e["cite"][:20])
+def test_golden(H, ex):
+    G = np.array(ex["G"], dtype=float)
+    Gp, info = run(H, G)
+    assert info.rank == ex["rank"]
+    assert np.abs(Gp - np.array(ex["Gp"], dtype=float) / ex["den"]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 5])
+def test_c1(H, seed):
+    G = I.make_single(I.CONFIGS["C1"], seed).numpy()
+    R = O.geninv(G)
+    assert R.in_Qstar()
+    Gp, info = run(H, G)
+    assert info.rank == R.rank == 32
+    assert C.rel_fro(Gp, R.Gp) <= REL
+    assert max(penrose_gpu(G, Gp)) <= PENROSE
+
+
+# r well below min(m, n): U V with a square factor is ill-conditioned (cond(G)^2 ~ 1e8..1e10),
+# where two correct FP64 implementations legitimately differ by more than 1e-9.
+@pytest.mark.parametrize("m,n,r", [(200, 130, 70), (130, 200, 70), (257, 255, 200), (1000, 333, 260),
+                                   (33, 700, 20), (520, 129, 1), (64, 64, 48), (2050, 530, 400)])
+def test_ragged_shapes(H, m, n, r):
+    seed = m * 31 + n
+    G = I.low_rank(seed, m, n, r).numpy()
+    R = O.geninv(G)
+    Gp, info = run(H, G)
+    assert info.transposed == (m < n)
+    assert info.rank == R.rank
+    if R.in_Q():
+        assert C.rel_fro(Gp, R.Gp) <= REL
+        assert max(penrose_gpu(G, Gp)) <= PENROSE
+    # decisions of the device match its own margins
+    assert info.tol == pytest.approx(R.tol, rel=1e-12)
+
+
+def test_c2_full_rank(H):
+    G = I.make_single(I.CONFIGS["C2"], 1).numpy()
+    R = O.geninv(G)
+    Gp, info = run(H, G)
+    assert info.rank == 1024
+    assert C.rel_fro(Gp, R.Gp) <= 1e-12
+    assert C.rel_fro(Gp, C.closed_form_full_rank(G)) <= 1e-12
+    assert max(penrose_gpu(G, Gp)) <= PENROSE
+
+
+def test_zero_and_nonfinite(H):
+    from paper_0804_4809_b200.binding import GeninvError, GENINV_ENONFINITE
+    Gp, info = run(H, np.zeros((40, 30)))
+    assert info.rank == 0 and np.all(Gp == 0)
+    G = np.ones((40, 30))
+    G[3, 4] = np.nan
+    with pytest.raises(GeninvError) as e:
+        run(H, G)
+    assert e.value.status == GENINV_ENONFINITE
+
+
+def test_determinism_and_ld(H):
+    G = I.low_rank(9, 700, 300, 250).numpy()
+    a, _ = run(H, G)
+    b, _ = run(H, G)
+    assert np.array_equal(a, b)
+    # leading dimensions larger than the width
+    Gd = torch.zeros(700, 310, dtype=torch.float64, device="cuda")
+    Gd[:, :300] = torch.as_tensor(G)
+    Gp = torch.full((300, 712), 7.0, dtype=torch.float64, device="cuda")
+    H.geninv_d(Gd[:, :300], Gp[:, :700])
+    assert np.array_equal(Gp[:, :700].cpu().numpy(), a)
+    assert torch.all(Gp[:, 700:] == 7.0)
+
+
+def test_host_buffers_match_device(H):
+    G = I.low_rank(12, 3000, 500, 350).numpy()
+    dev_gp, dev_info = run(H, G)
+    Gh = torch.as_tensor(G).pin_memory()
+    Gph = torch.empty(500, 3000, dtype=torch.float64).pin_memory()
+    _, info = H.geninv_host_d(Gh, Gph)
+    assert info.rank == dev_info.rank
+    assert C.rel_fro(Gph.numpy(), dev_gp) <= 1e-12
+    Gt = np.ascontiguousarray(G.T)
+    Gth = torch.as_tensor(Gt).pin_memory()
+    Gpth = torch.empty(3000, 500, dtype=torch.float64).pin_memory()
+    _, info = H.geninv_host_d(Gth, Gpth)
+    assert info.rank == dev_info.rank and info.transposed
+    assert C.rel_fro(Gpth.numpy(), dev_gp.T) <= 1e-10
+
+
+def test_split_api_equals_whole(H):
+    G = I.low_rank(13, 1500, 400, 300).numpy()
+    whole, info = run(H, G)
+    Gd = to_dev(G)
+    A = torch.zeros(400, 400, dtype=torch.float64, device="cuda")
+    for rows in (slice(0, 700), slice(700, 1500)):      # two "row shards" summed by hand
+        Ap = torch.zeros_like(A)
+        H.geninv_gram_d(Gd[rows], 0, Ap)
+        A += Ap
+    inf2 = H.geninv_from_gram_d(A)
+    assert inf2.rank == info.rank
+    Gp = torch.empty(400, 1500, dtype=torch.float64, device="cuda")
+    H.geninv_apply_d(Gd[0:700], 0, Gp[:, 0:700])
+    H.geninv_apply_d(Gd[700:1500], 0, Gp[:, 700:1500])
+    torch.cuda.synchronize()
+    # the sharded Gram sums in a different order: same rank, both within the oracle gate
+    R = O.geninv(G)
+    assert R.in_Q() and inf2.rank == R.rank
+    assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= REL
+    assert C.rel_fro(whole, R.Gp) <= REL
+
+
+@pytest.mark.slow
+def test_c3_both_orientations(H):
+    cfg = I.CONFIGS["C3"]
+    G = I.make_single(cfg, 1, device="cuda")
+    Gh = G.cpu().numpy()
+    R = O.geninv(Gh)
+    Gp, info = H.geninv_d(G)
+    assert info.transposed and info.rank == R.rank == 3072
+    assert R.in_Q()
+    Gpn = Gp.cpu().numpy()
+    assert C.rel_fro(Gpn, R.Gp) <= REL
+    D, S = I.copy_columns(1, cfg.n, cfg.ncopy)
+    assert np.array_equal(Gpn[D], Gpn[S])                # R13: duplicated columns -> equal rows
+    Gt = G.T.contiguous()
+    Gpt, info_t = H.geninv_d(Gt)
+    assert not info_t.transposed and info_t.rank == 3072
+    assert C.rel_fro(Gpt.cpu().numpy().T, Gpn) <= REL    # (G')+ = (G+)'
+    assert max(penrose_gpu(Gh, Gpn)) <= PENROSE
+
+
+def test_c5_batched_slice(H):
+    cfg = I.CONFIGS["C5"]
+    nb = 2048
+    Gb = I.make_batch(cfg, 5, 0, nb, device="cuda")
+    Gp, rank = H.geninv_batched_d(Gb)
+    torch.cuda.synchronize()
+    Gpo, ro, mu_acc, mu_drop = O.geninv_batched(Gb.cpu().numpy())
+    rk = rank.cpu().numpy()
+    q = (mu_acc >= 1e4) & (mu_drop <= 1e-2)
+    qs = (mu_acc >= 1e6) & (mu_drop <= 1e-3)
+    assert q.mean() > 0.9
+    assert np.array_equal(rk[q], ro[q])
+    G_ = Gb.cpu().numpy()
+    Gp_ = Gp.cpu().numpy()
+    for b in np.nonzero(q)[0]:
+        assert C.rel_fro(Gp_[b], Gpo[b]) <= REL, b
+    for b in np.nonzero(qs)[0][:256]:
+        assert max(penrose_gpu(G_[b], Gp_[b])) <= PENROSE, b
+
+
+def test_c1_batched_matches_single(H):
+    cfg = I.CONFIGS["C1"]
+    Gs = torch.stack([I.make_single(cfg, s) for s in (1, 2, 3)]).cuda()
+    Gp, rank = H.geninv_batched_d(Gs)
+    torch.cuda.synchronize()
+    for i, s in enumerate((1, 2, 3)):
+        R = O.geninv(Gs[i].cpu().numpy())
+        assert int(rank[i]) == R.rank
+        assert C.rel_fro(Gp[i].cpu().numpy(), R.Gp) <= REL
+    # transposed small shapes and ragged sizes through the batched kernel
+    G2 = torch.stack([I.low_rank(s, 40, 90, 17) for s in range(5)]).cuda()
+    Gp2, r2 = H.geninv_batched_d(G2)
+    torch.cuda.synchronize()
+    for i in range(5):
+        R = O.geninv(G2[i].cpu().numpy())
+        assert int(r2[i]) == R.rank == 17
+        assert C.rel_fro(Gp2[i].cpu().numpy(), R.Gp) <= REL
