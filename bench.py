@@ -1,0 +1,507 @@
+"""bench.py -- geninv FP64 throughput on B200 (the BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4|C3T|C3|C2|C5] [--impl ours|reference]
+
+Default workload: C4, the tall 2,097,152 x 4096 matrix of exact rank 3584
+(BASELINE.json configs[3]), rows sharded over the N ranks: each rank forms
+its partial Gram G_p'G_p, one NCCL all-reduce sums A, the factorisation and
+inverse run replicated, and each rank writes its own column block of G+
+(SURVEY §8(e)).  One step = one whole geninv of the workload (a1-a8).
+Total work is fixed as N grows ("scaling": "strong").
+
+value      = F_alg / (max-over-ranks device time per step), GFLOP/s, inputs resident in HBM
+e2e        = the same through the C ABI with HOST buffers (pinned), copies inside the timed region
+roofline   = the dominant kernel (the a7 output product, DMMA) against the measured FP64 DMMA peak
+cpu_baseline = the oracle (numpy, paper's algorithm) on a bounded row sample of the same workload
+
+--impl reference times the oracle itself (the deliberately slow CPU reference) on that sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_0804_4809_b200 import inputs as I  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "MEASURED_FP64.json")
+SEED = 1
+
+
+# --------------------------------------------------------------------------- flop model
+def f_alg(s: int, ell: int, piv: np.ndarray) -> dict:
+    """Algorithmic FP64 flops of one geninv (SURVEY §8(a) convention: SYRKs count one triangle)."""
+    r = len(piv)
+    k = np.arange(s)
+    rk = np.searchsorted(np.sort(piv), k, side="left")      # columns accepted before column k
+    chol = float(np.sum(2.0 * (s - k) * rk + (s - k)))
+    parts = {
+        "gram": float(ell) * s * (s + 1),
+        "chol": chol,
+        "ltl": float(s) * r * (r + 1),
+        "inv": float(r) ** 3,
+        "kx": 2.0 * s * r * r + float(s) * (s + 1) * r,
+        "out": 2.0 * s * s * ell,
+    }
+    parts["total"] = sum(parts.values())
+    return parts
+
+
+def fp64_peak():
+    try:
+        d = json.load(open(FP64_PEAK_FILE))
+        return d["dmma_tflops"], "measured (profiles/MEASURED_FP64.json: register-resident DMMA.8x8x4 microbenchmark)"
+    except Exception:
+        return 37.2, "nominal 148 SM x 128 flop/clk x 1.965 GHz (no measured FP64 peak file)"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- distributed
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        if world == 1 and n_gpus > 1:
+            raise SystemExit(f"--gpus {n_gpus} needs torchrun --nproc-per-node {n_gpus}")
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def allmax(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------- workloads
+def workload(name: str):
+    if name == "C4":
+        return I.CONFIGS["C4"], False, "C4: tall G 2097152 x 4096 fp64, exact rank 3584 (U V, N(0,1)), rows sharded"
+    if name == "C3T":
+        c = I.CONFIGS["C3"]
+        return I.Config("C3T", c.n, c.m, c.rank, ncopy=c.ncopy), True, \
+            "C3 transposed: G' of the 4096 x 16384 rank-3072 matrix, i.e. 16384 x 4096 (N branch)"
+    if name in ("C1", "C2", "C3", "C5"):
+        return I.CONFIGS[name], False, f"{name}: BASELINE.json configs"
+    raise SystemExit(f"unknown workload {name}")
+
+
+def make_rows(cfg, transposed_of_c3, row0, rows, device):
+    if transposed_of_c3:
+        c3 = I.CONFIGS["C3"]
+        G = I.make_single(c3, SEED, device=device)
+        return G.T[row0:row0 + rows].contiguous()
+    return I.make_single(cfg, SEED, device=device, row0=row0, rows=rows)
+
+
+# --------------------------------------------------------------------------- the reference arm (oracle)
+def oracle_sample(cfg, transposed_of_c3):
+    """A bounded sample of the workload for the CPU oracle: its first rows (C4: 16384 of 2^21 rows)."""
+    if cfg.name in ("C4",):
+        rows = 16384
+        G = I.make_single(cfg, SEED, rows=rows).numpy()
+        return G, f"rows 0..{rows - 1} of the C4 matrix ({rows} x {cfg.n}, same generator, N branch)"
+    if transposed_of_c3 or cfg.name == "C3":
+        c3 = I.CONFIGS["C3"]
+        cols = 4096
+        G = I.make_single(c3, SEED).numpy()
+        G = G.T[:cols] if transposed_of_c3 else G[:, :cols].copy()
+        return np.ascontiguousarray(G), f"{cols} of 16384 long-side lines of C3"
+    if cfg.name == "C5":
+        G = I.make_batch(cfg, SEED, 0, 512).numpy()
+        return G, "matrices 0..511 of the 65536-matrix batch"
+    G = I.make_single(cfg, SEED).numpy()
+    return G, "the whole matrix"
+
+
+def run_oracle_once(G):
+    from oracle import geninv_oracle as O
+    t0 = time.perf_counter()
+    if G.ndim == 3:
+        Gp, r, _, _ = O.geninv_batched(G)
+        dt = time.perf_counter() - t0
+        m, n = G.shape[1:]
+        s, ell = min(m, n), max(m, n)
+        fl = sum(f_alg(s, ell, np.arange(int(rv)))["total"] for rv in r)  # rank-r leading columns (approx.)
+        return fl, dt
+    R = O.geninv(G)
+    dt = time.perf_counter() - t0
+    m, n = G.shape
+    fl = f_alg(min(m, n), max(m, n), R.chol.piv)["total"]
+    return fl, dt
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def reference_arm(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, tr, desc = workload(args.workload)
+    G, sample = oracle_sample(cfg, tr)
+    for _ in range(args.warmup):
+        run_oracle_once(G)
+    fl_tot, dt_tot = 0.0, 0.0
+    for _ in range(args.steps):
+        fl, dt = run_oracle_once(G)
+        fl_tot += fl
+        dt_tot += dt
+    v = fl_tot / dt_tot / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt_tot / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    from paper_0804_4809_b200.binding import Handle
+
+    world, rank, local = dist_setup(args.gpus)
+    cfg, c3t, desc = workload(args.workload)
+    if cfg.batch > 1:
+        return bench_batched(args, cfg, desc, world, rank)
+    m, n = cfg.m, cfg.n
+    tr = int(m < n)
+    s, ell = min(m, n), max(m, n)
+    if world > 1 and tr:
+        raise SystemExit("row sharding applies to the tall (N-branch) configs only")
+    rows = m // world
+    row0 = rank * rows
+    if rank == world - 1:
+        rows = m - row0
+    dev = torch.device("cuda", local)
+
+    # ---- inputs resident in HBM
+    G = make_rows(cfg, c3t, row0, rows, dev) if world > 1 or not c3t else make_rows(cfg, c3t, 0, m, dev)
+    Gp = torch.empty(n, rows, dtype=torch.float64, device=dev)   # local column block of G+ (n x rows)
+    A = torch.zeros(s, s, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    h = Handle(local)
+    stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        import torch.distributed as dist
+
+    ev_out = []
+
+    def step(record=False):
+        if world > 1:
+            h.geninv_gram_d(G, 0, A)
+            dist.all_reduce(A)                       # a8: A = sum_p G_p'G_p over NVLink
+            info = h.geninv_from_gram_d(A)
+        elif tr:
+            info = None
+        else:
+            h.geninv_gram_d(G, 0, A)
+            info = h.geninv_from_gram_d(A)
+        if tr:                                       # T branch (single GPU): whole call
+            _, info = h.geninv_d(G, Gp)
+            return info
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        h.geninv_apply_d(G, 0, Gp)
+        if record:
+            e1.record(stream)
+            ev_out.append((e0, e1))
+        return info
+
+    info = step()
+    torch.cuda.synchronize()
+    # piv for the flop model (untimed): the full-rank Cholesky of the same A
+    if not tr:
+        _, piv, _ = h.geninv_frchol_d(A)
+        piv = piv.cpu().numpy()
+    else:
+        Aw = torch.zeros(s, s, dtype=torch.float64, device=dev)
+        h.geninv_gram_d(G, 1, Aw)
+        _, piv, _ = h.geninv_frchol_d(Aw)
+        piv = piv.cpu().numpy()
+        del Aw
+    F = f_alg(s, ell, piv)
+    for _ in range(max(0, args.warmup - 1)):
+        step()
+    barrier(world)
+    l0 = h.launch_count
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            info = step(record=True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = (h.launch_count - l0) * world + (args.steps * world if world > 1 else 0)  # + NCCL all-reduce
+    ms = t0.elapsed_time(t1) / args.steps
+    ms = allmax(ms, world)
+    value = F["total"] / (ms * 1e-3) / 1e9
+    peak, peak_src = fp64_peak()
+    # dominant kernel: a7 output product, one launch per step per rank
+    if ev_out:
+        out_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_out]))
+        out_ms = allmax(out_ms, world)
+        out_flops_launch = 2.0 * s * s * rows
+        achieved = out_flops_launch / (out_ms * 1e-3) / 1e12
+    else:
+        out_ms, achieved, out_flops_launch = None, None, None
+    traffic = None
+    try:
+        tr_d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr_d.get(f"{args.workload}_out_bytes_per_launch")
+    except Exception:
+        pass
+    rank_ok = info.rank if info is not None else None
+    clocks = clk.summary()
+
+    # ---- free the device-resident inputs before the host-buffer (e2e) run
+    del G, Gp
+    torch.cuda.empty_cache()
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, cfg, c3t, world, rank, local, row0, rows, F, h)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Gs, sample = oracle_sample(cfg, c3t)
+        fl, dt = run_oracle_once(Gs)                      # warm (BLAS threads, page-in)
+        fl, dt = run_oracle_once(Gs)
+        cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": sample + f"; oracle = numpy/OpenBLAS geninv of PAPER.md P:105-140, {dt:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": SEED,
+                       "ms_per_matrix": ms, "parallelism": f"rows sharded x{world}" if world > 1 else "single GPU",
+                       "pct_fp64_peak": value / (peak * 1e3), "flops_per_step": F["total"],
+                       "flops_breakdown": {k: v for k, v in F.items() if k != "total"},
+                       "l2": "inputs (G 64 GiB) far larger than the 126 MB L2; no flush needed"
+                       if cfg.name == "C4" else "inputs larger than L2" if m * n * 8 > 126e6 else
+                       "inputs smaller than L2 (not flushed)"},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "dgemm_tc<128,128,64,32,4,K-major,K-major> (a7 G+ = X G')",
+                         "flops_per_launch": out_flops_launch, "ms_per_launch": out_ms,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_run(args, cfg, c3t, world, rank, local, row0, rows, F, h):
+    """Same metric through the C ABI with host buffers: H2D of G and D2H of G+ inside the timed region."""
+    m, n = cfg.m, cfg.n
+    dev = torch.device("cuda", local)
+    try:
+        Gh = torch.empty(rows, n, dtype=torch.float64).pin_memory()
+        Gph = torch.empty(n, rows, dtype=torch.float64).pin_memory()
+    except RuntimeError as e:
+        return {"value": None, "unit": "GFLOP/s", "skipped": f"pinned host buffers unavailable: {e}"[:200]}
+    # fill the host input from the same generator (device-side generation, copied once, untimed)
+    chunk = 1 << 16
+    for c0 in range(0, rows, chunk):
+        c1 = min(rows, c0 + chunk)
+        if c3t:
+            blk = make_rows(cfg, c3t, row0 + c0, c1 - c0, dev)
+        else:
+            blk = I.make_single(cfg, SEED, device=dev, row0=row0 + c0, rows=c1 - c0)
+        Gh[c0:c1].copy_(blk)
+        del blk
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        import torch.distributed as dist
+        Gd = torch.empty(rows, n, dtype=torch.float64, device=dev)
+        Gpd = torch.empty(n, rows, dtype=torch.float64, device=dev)
+        A = torch.zeros(n, n, dtype=torch.float64, device=dev)
+
+        def step():
+            Gd.copy_(Gh, non_blocking=True)
+            h.geninv_gram_d(Gd, 0, A)
+            dist.all_reduce(A)
+            h.geninv_from_gram_d(A)
+            h.geninv_apply_d(Gd, 0, Gpd)
+            Gph.copy_(Gpd, non_blocking=True)
+            torch.cuda.synchronize()
+    else:
+        def step():
+            h.geninv_host_d(Gh, Gph)
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    barrier(world)
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / args.steps * 1e3
+    barrier(world)
+    ms = allmax(wall, world)
+    return {"value": F["total"] / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(m) * n * 8, "d2h_bytes_per_step": int(m) * n * 8,
+            "api": "geninv_host_d (pinned host G and G+)" if world == 1 else
+            "pinned H2D + geninv_gram_d / all_reduce / geninv_from_gram_d / geninv_apply_d + D2H"}
+
+
+def bench_batched(args, cfg, desc, world, rank):
+    from paper_0804_4809_b200.binding import Handle
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    nb = cfg.batch // world
+    b0 = rank * nb
+    G = I.make_batch(cfg, SEED, b0, nb, device=dev)
+    Gp = torch.empty(nb, cfg.n, cfg.m, dtype=torch.float64, device=dev)
+    rk = torch.empty(nb, dtype=torch.int32, device=dev)
+    h = Handle(local)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        h.geninv_batched_d(G, Gp, rk)
+    barrier(world)
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            h.geninv_batched_d(G, Gp, rk)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = allmax(e0.elapsed_time(e1) / args.steps, world)
+    s, ell = min(cfg.m, cfg.n), max(cfg.m, cfg.n)
+    ranks = rk.cpu().numpy()
+    F = sum(f_alg(s, ell, np.arange(int(r)))["total"] for r in ranks) * world
+    peak, src = fp64_peak()
+    value = F / (ms * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic",
+                          "config": {"workload": desc, "batch": cfg.batch, "us_per_matrix": ms * 1e3 / cfg.batch,
+                                     "hbm_gbs": 2 * cfg.batch * cfg.m * cfg.n * 8 / (ms * 1e-3) / 1e9},
+                          "clocks": clk.summary(),
+                          "roofline": {"bound": "tensor", "achieved": value / 1e3, "peak": peak, "unit": "TFLOP/s",
+                                       "frac": value / 1e3 / peak, "traffic": None, "peak_source": src},
+                          "gpu_launches": args.steps}), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
