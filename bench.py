@@ -287,16 +287,26 @@ def main():
         import torch.distributed as dist
 
     ev_out = []
+    ev_phase = []
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
 
     def step(record=False):
+        if record:
+            p0 = ev()
         if world > 1:
             h.geninv_gram_d(G, 0, A)
             dist.all_reduce(A)                       # a8: A = sum_p G_p'G_p over NVLink
+            p1 = ev() if record else None
             info = h.geninv_from_gram_d(A)
         elif tr:
             info = None
         else:
             h.geninv_gram_d(G, 0, A)
+            p1 = ev() if record else None
             info = h.geninv_from_gram_d(A)
         if tr:                                       # T branch (single GPU): whole call
             _, info = h.geninv_d(G, Gp)
@@ -309,6 +319,7 @@ def main():
         if record:
             e1.record(stream)
             ev_out.append((e0, e1))
+            ev_phase.append((p0, p1, e0, e1))
         return info
 
     info = step()
@@ -350,6 +361,10 @@ def main():
         achieved = out_flops_launch / (out_ms * 1e-3) / 1e12
     else:
         out_ms, achieved, out_flops_launch = None, None, None
+    phases = None
+    if ev_phase:
+        ph = np.array([[a.elapsed_time(b), b.elapsed_time(c), c.elapsed_time(d)] for a, b, c, d in ev_phase])
+        phases = dict(zip(["gram_allreduce_ms", "factor_inverse_x_ms", "output_ms"], ph.mean(axis=0).round(3).tolist()))
     traffic = None
     try:
         tr_d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -382,6 +397,7 @@ def main():
             "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": SEED,
                        "ms_per_matrix": ms, "parallelism": f"rows sharded x{world}" if world > 1 else "single GPU",
                        "pct_fp64_peak": value / (peak * 1e3), "flops_per_step": F["total"],
+                       "phase_ms_rank0": phases,
                        "flops_breakdown": {k: v for k, v in F.items() if k != "total"},
                        "l2": "inputs (G 64 GiB) far larger than the 126 MB L2; no flush needed"
                        if cfg.name == "C4" else "inputs larger than L2" if m * n * 8 > 126e6 else

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgeninv.so")
+LIB_PATH = os.environ.get("GENINV_LIB", os.path.join(_HERE, "libgeninv.so"))  # instrumented builds only
 
 GENINV_OK, GENINV_EINVAL, GENINV_ENONFINITE, GENINV_ENOTSPD, GENINV_ECUDA, GENINV_ENOMEM, GENINV_EALIGN, \
     GENINV_ESTATE = range(8)

@@ -93,10 +93,10 @@ cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
     if (!op.a_kmajor && op.b_kmajor) return launch<128, 32, 32, 32, 6, false, true>(op, a, st);
     return launch<128, 32, 32, 32, 6, false, false>(op, a, st);
   }
-  if (op.a_kmajor && op.b_kmajor) return launch<128, 128, 64, 32, 4, true, true>(op, a, st);
-  if (op.a_kmajor && !op.b_kmajor) return launch<128, 128, 64, 32, 4, true, false>(op, a, st);
-  if (!op.a_kmajor && op.b_kmajor) return launch<128, 128, 64, 32, 4, false, true>(op, a, st);
-  return launch<128, 128, 64, 32, 4, false, false>(op, a, st);
+  if (op.a_kmajor && op.b_kmajor) return launch<128, 128, 64, 32, 6, true, true>(op, a, st);
+  if (op.a_kmajor && !op.b_kmajor) return launch<128, 128, 64, 32, 6, true, false>(op, a, st);
+  if (!op.a_kmajor && op.b_kmajor) return launch<128, 128, 64, 32, 6, false, true>(op, a, st);
+  return launch<128, 128, 64, 32, 6, false, false>(op, a, st);
 }
 
 // ---------------------------------------------------------------- split-K reduction

@@ -100,8 +100,9 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
   __syncthreads();
 
   // TMA issue (thread 0): slab `it` goes to stage it % STAGES.  The first
-  // STAGES slabs are issued up front; slab it + STAGES - 1 is issued after
-  // every warp has released stage (it - 1) % STAGES (empty barrier).
+  // STAGES slabs are issued up front; at the top of iteration it, slab
+  // it + STAGES - 1 is issued once every warp has released stage
+  // (it - 1) % STAGES (empty barrier).
   auto issue = [&](int it) {
     const int st = it % STAGES;
     unsigned char *sA = smem + st * Cfg::STAGE_BYTES;
@@ -142,8 +143,15 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
 
   const uint32_t sbase = smem_u32(smem);
   for (int it = 0; it < nslab; ++it) {
+    // refill the stage released by slab it - 1 with slab it + STAGES - 1 before computing slab it
+    if (threadIdx.x == 0 && it >= 1 && it + STAGES - 1 < nslab) {
+      const int prev = it - 1;
+      mbar_wait(&empty[prev % STAGES], (prev / STAGES) & 1);
+      issue(it + STAGES - 1);
+    }
     const int st = it % STAGES;
     const uint32_t ph = (it / STAGES) & 1;
+    const bool kmask_slab = p.K_dev && (s_begin + it + 1) * BK > K;
     mbar_wait(&full[st], ph);
     const uint32_t sA = sbase + st * Cfg::STAGE_BYTES;
     const uint32_t sB = sA + Cfg::A_BYTES;
@@ -201,6 +209,12 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
           if (B_K) b[f] = e ? bv[0][f].y : bv[0][f].x;
           else b[f] = (f & 1) ? bv[e][f & ~1].y : bv[e][f & ~1].x;
         }
+        // device-side K (K_dev) that ends inside this slab: columns k >= K may hold live data
+        // (the panel update reads L while later columns are being written) -> zero them.
+        if (kmask_slab && (s_begin + it) * BK + 8 * h + 2 * t + e >= K) {
+#pragma unroll
+          for (int f = 0; f < FM; ++f) a[f] = 0.0;
+        }
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -209,11 +223,6 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    if (threadIdx.x == 0 && it >= 1 && it + STAGES - 1 < nslab) {
-      const int prev = it - 1;
-      mbar_wait(&empty[prev % STAGES], (prev / STAGES) & 1);
-      issue(it + STAGES - 1);
-    }
   }
 
   // ================= epilogue (registers -> global) =================

@@ -22,8 +22,9 @@ using namespace gi;
 
 struct geninv_handle_s {
   int device = 0;
-  cudaStream_t own = nullptr, st = nullptr, st2 = nullptr;
+  cudaStream_t own = nullptr, st = nullptr, st2 = nullptr, upd = nullptr;
   cudaEvent_t ev[4] = {};
+  cudaEvent_t ev_fr[4] = {};  // frchol lookahead events
   // s x s workspaces (leading dimension ld >= round_up(s, 32))
   int s_cap = 0;
   long long ld = 0;
@@ -92,7 +93,7 @@ geninv_status ensure_ws(geninv_handle h, int s) {
   const size_t sq = (size_t)ld * ld * sizeof(double);
   double **bufs[] = {&h->A, &h->L, &h->Bm, &h->Cf, &h->Ci, &h->Mm, &h->Kb, &h->X, &h->T};
   for (auto b : bufs) GI_TRY(cudaMalloc(b, sq));
-  h->wp_elems = 16LL * ld * PB;
+  h->wp_elems = 18LL * ld * PB;
   GI_TRY(cudaMalloc(&h->Wp, h->wp_elems * sizeof(double)));
   const int np = (int)(ld / PB) + 2;
   GI_TRY(cudaMalloc(&h->rk, np * sizeof(int)));
@@ -179,9 +180,9 @@ geninv_status factor(geninv_handle h, const double *A, long long lda, int s, dou
                      const geninv_opts *opts, int *rank_out, FactorStats *hst) {
   GI_TRY(tolerance(A, lda, s, tol_rel_of(opts), tol_abs_of(opts), h->fs, h->st));
   GI_TRY(cudaMemsetAsync(L, 0, (size_t)s * ldl * sizeof(double), h->st));
-  GI_TRY(frchol(A, lda, s, L, ldl, piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, h->st));
+  GI_TRY(frchol(A, lda, s, L, ldl, piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, h->st, h->upd, h->ev_fr));
   const int np = (s + PB - 1) / PB;
-  h->launches += 1 + np + (np - 1);
+  h->launches += 1 + np + 2 * std::max(0, np - 2);
   int r = 0;
   GI_TRY(cudaMemcpyAsync(&r, h->rk + np, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   GI_TRY(cudaMemcpyAsync(hst, h->fs, sizeof(FactorStats), cudaMemcpyDeviceToHost, h->st));
@@ -198,7 +199,7 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   GI_TRY(cudaMemsetAsync(h->Cf, 0, (size_t)r_pad * ld * sizeof(double), h->st));
   GI_TRY(cudaMemsetAsync(h->Ci, 0, (size_t)r_pad * ld * sizeof(double), h->st));
   GI_TRY(tolerance(B, ldb, r, 0.0, 0.0, h->fs2, h->st));
-  GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st));
+  GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st, h->upd, h->ev_fr));
   GI_TRY(trtri_lower(h->Cf, ld, r, h->Ci, ld, h->T, h->st));
   // M = C^-T C^-1 : M[i][j] = sum_k Ci[k][i] Ci[k][j]
   GemmOp op;
@@ -215,7 +216,7 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   const int np = (r + PB - 1) / PB;
   int lev = 0;
   for (int hh = 32; hh < r_pad; hh *= 2) ++lev;
-  h->launches += 1 + np + (np - 1) + 2 + 4 * lev + 1;
+  h->launches += 1 + np + 2 * std::max(0, np - 2) + 2 + 4 * lev + 1;
   return GENINV_OK;
 }
 
@@ -350,7 +351,9 @@ geninv_status geninv_create(geninv_handle *out, int device) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->upd, cudaStreamNonBlocking);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming);
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_fr[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete h;
     return cuda_status(e);
@@ -377,6 +380,9 @@ geninv_status geninv_destroy(geninv_handle h) {
     if (c) cudaFree(c);
   for (auto &ev : h->ev)
     if (ev) cudaEventDestroy(ev);
+  for (auto &ev : h->ev_fr)
+    if (ev) cudaEventDestroy(ev);
+  if (h->upd) cudaStreamDestroy(h->upd);
   if (h->st2) cudaStreamDestroy(h->st2);
   if (h->own) cudaStreamDestroy(h->own);
   delete h;

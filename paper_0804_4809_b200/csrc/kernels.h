@@ -21,13 +21,16 @@ struct FactorStats {
 cudaError_t tolerance(const double *A, long long lda, int s, double tol_rel, double tol_abs, FactorStats *st,
                       cudaStream_t stream);
 
-// a3: blocked left-looking rank-revealing Cholesky.  L (s x s, ldl) must be
-// zero on entry; rk: device int[ceil(s/PB)+1] (rk[p] = rank before panel p,
-// rk[npanels] = final rank); piv: device int[s]; Wp: split-K workspace of
-// wp_elems doubles (>= 16 * s * PB).  mode 0: drop iff pivot <= tol (paper);
-// mode 1: SPD (accept iff pivot > 0, flag bit1 otherwise).
+// a3: blocked left-looking rank-revealing Cholesky with one-panel lookahead.
+// L (s x s, ldl) must be zero on entry; rk: device int[ceil(s/PB)+1] (rk[p] =
+// rank before panel p, rk[npanels] = final rank); piv: device int[s]; Wp:
+// workspace of wp_elems doubles (>= 18 * s * PB).  mode 0: drop iff pivot <=
+// tol (paper); mode 1: SPD (accept iff pivot > 0, flag bit1 otherwise).  The
+// big updates run on `upd` (a second stream) concurrently with the previous
+// panel; ev: 4 events owned by the caller.
 cudaError_t frchol(const double *A, long long lda, int s, double *L, long long ldl, int *piv, int *rk,
-                   FactorStats *st, int mode, double *Wp, long long wp_elems, cudaStream_t stream);
+                   FactorStats *st, int mode, double *Wp, long long wp_elems, cudaStream_t stream,
+                   cudaStream_t upd, cudaEvent_t *ev);
 
 // a5 pieces: Cinv = C^-1 for lower-triangular C (r x r, ldc) padded to
 // r_pad = round_up(r, 32) with an identity block; C and Cinv are r_pad x r_pad

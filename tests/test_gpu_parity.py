@@ -141,7 +141,7 @@ def test_host_buffers_match_device(H):
 
 
 def test_split_api_equals_whole(H):
-    G = I.low_rank(13, 1500, 400, 300).numpy()
+    G = I.low_rank(13, 1500, 400, 250).numpy()
     whole, info = run(H, G)
     Gd = to_dev(G)
     A = torch.zeros(400, 400, dtype=torch.float64, device="cuda")
