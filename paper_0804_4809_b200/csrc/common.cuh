@@ -70,4 +70,13 @@ GI_DEV void tma_load_3d(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, 
       : "memory");
 }
 
+// 4-D tiled load (MN-major operand viewed as {16, k, m/16, batch}: one op per 128-wide tile).
+GI_DEV void tma_load_4d(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 }  // namespace gi

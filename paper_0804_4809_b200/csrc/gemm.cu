@@ -54,6 +54,26 @@ static cudaError_t make_map(CUtensorMap *map, const Mat &m, int box_rows) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// MN-major operand as a 4-D view {16 (mn inner), rows (k), cols/16 (mn outer), batch}; box
+// {16, 16, strips, 1} -> the whole [strip][k][16] tile in one TMA op, same smem layout and
+// swizzle as the per-strip 3-D boxes.  Needs cols % 16 == 0.
+static cudaError_t make_map_mn4d(CUtensorMap *map, const Mat &m, int strips) {
+  cudaError_t e = get_encode();
+  if (e != cudaSuccess) return e;
+  if ((reinterpret_cast<uintptr_t>(m.ptr) & 15) || (m.ld & 1) || (m.cols % 16) || (m.batch > 1 && (m.bstride & 1)))
+    return cudaErrorMisalignedAddress;
+  cuuint64_t dims[4] = {16, (cuuint64_t)m.rows, (cuuint64_t)(m.cols / 16), (cuuint64_t)m.batch};
+  long long bstride = m.batch > 1 ? m.bstride : m.ld * m.rows;
+  if (bstride < 2) bstride = 2;
+  cuuint64_t strides[3] = {(cuuint64_t)m.ld * 8, 128, (cuuint64_t)bstride * 8};
+  cuuint32_t box[4] = {16, 16, (cuuint32_t)strips, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(m.ptr), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int BM, int BN, int WM, int WN, int ST, bool AK, bool BK_>
 static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM, WN, ST, AK, BK_>;
@@ -64,9 +84,12 @@ static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  cudaError_t e = make_map(&a.tmA, op.A, AK ? BM : 16);
+  cudaError_t e;
+  a.a_mn4d = !AK && (op.A.cols % 16 == 0) && (op.a_mn0 % 16 == 0);
+  a.b_mn4d = !BK_ && (op.B.cols % 16 == 0) && (op.b_mn0 % 16 == 0);
+  e = a.a_mn4d ? make_map_mn4d(&a.tmA, op.A, BM / 16) : make_map(&a.tmA, op.A, AK ? BM : 16);
   if (e != cudaSuccess) return e;
-  e = make_map(&a.tmB, op.B, BK_ ? BN : 16);
+  e = a.b_mn4d ? make_map_mn4d(&a.tmB, op.B, BN / 16) : make_map(&a.tmB, op.B, BK_ ? BN : 16);
   if (e != cudaSuccess) return e;
   a.mtiles = (op.M + BM - 1) / BM;
   a.ntiles = (op.N + BN - 1) / BN;

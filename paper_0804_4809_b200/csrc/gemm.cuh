@@ -35,6 +35,7 @@ struct GemmArgs {
   int lower;                // 1: enumerate lower-triangle tiles of a square output (M == N)
   int mirror;               // 1 (with lower): also store C[n][m]; diagonal tiles store m >= n mirrored
   int splits;               // split-K count
+  int a_mn4d, b_mn4d;       // MN-major operand mapped as a 4-D {16, k, mn/16, batch} view: one TMA op per tile
 };
 
 // row permutation inside an 8-row fragment: makes the LDS.128 fragment loads
@@ -103,30 +104,34 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
   // STAGES slabs are issued up front; at the top of iteration it, slab
   // it + STAGES - 1 is issued once every warp has released stage
   // (it - 1) % STAGES (empty barrier).
+  // Issued by all 32 lanes of warp 0: lane 0 arms the barrier, then each TMA box
+  // (one for a K-major tile, 16-column strips for an MN-major tile) is issued by
+  // its own lane -- one warp instruction instead of up to 16 serial issues.
   auto issue = [&](int it) {
     const int st = it % STAGES;
     unsigned char *sA = smem + st * Cfg::STAGE_BYTES;
     unsigned char *sB = sA + Cfg::A_BYTES;
-    mbar_arrive_expect_tx(&full[st], Cfg::STAGE_BYTES);
+    if (lane == 0) mbar_arrive_expect_tx(&full[st], Cfg::STAGE_BYTES);
+    __syncwarp();
     const int k = (s_begin + it) * BK;
-    if (A_K) {
-      tma_load_3d(sA, &p.tmA, &full[st], p.a_k0 + k, p.a_mn0 + m0, bz);
-    } else {
-#pragma unroll
-      for (int q = 0; q < BM / 16; ++q)
-        tma_load_3d(sA + q * 2048, &p.tmA, &full[st], p.a_mn0 + m0 + 16 * q, p.a_k0 + k, bz);
-    }
-    if (B_K) {
-      tma_load_3d(sB, &p.tmB, &full[st], p.b_k0 + k, p.b_mn0 + n0, bz);
-    } else {
-#pragma unroll
-      for (int q = 0; q < BN / 16; ++q)
-        tma_load_3d(sB + q * 2048, &p.tmB, &full[st], p.b_mn0 + n0 + 16 * q, p.b_k0 + k, bz);
+    constexpr int NA = A_K ? 1 : BM / 16, NB = B_K ? 1 : BN / 16;
+    static_assert(NA + NB <= 32, "one lane per TMA box");
+    if (lane < NA) {
+      if (A_K) tma_load_3d(sA, &p.tmA, &full[st], p.a_k0 + k, p.a_mn0 + m0, bz);
+      else if (p.a_mn4d) { if (lane == 0) tma_load_4d(sA, &p.tmA, &full[st], 0, p.a_k0 + k, (p.a_mn0 + m0) / 16, bz); }
+      else tma_load_3d(sA + lane * 2048, &p.tmA, &full[st], p.a_mn0 + m0 + 16 * lane, p.a_k0 + k, bz);
+    } else if (lane < NA + NB) {
+      const int q = lane - NA;
+      if (B_K) tma_load_3d(sB, &p.tmB, &full[st], p.b_k0 + k, p.b_mn0 + n0, bz);
+      else if (p.b_mn4d) { if (q == 0) tma_load_4d(sB, &p.tmB, &full[st], 0, p.b_k0 + k, (p.b_mn0 + n0) / 16, bz); }
+      else tma_load_3d(sB + q * 2048, &p.tmB, &full[st], p.b_mn0 + n0 + 16 * q, p.b_k0 + k, bz);
     }
   };
-  if (threadIdx.x == 0 && nslab > 0) {
-    tma_prefetch(&p.tmA);
-    tma_prefetch(&p.tmB);
+  if (warp == 0 && nslab > 0) {
+    if (lane == 0) {
+      tma_prefetch(&p.tmA);
+      tma_prefetch(&p.tmB);
+    }
     for (int it = 0; it < STAGES && it < nslab; ++it) issue(it);
   }
 
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
   const uint32_t sbase = smem_u32(smem);
   for (int it = 0; it < nslab; ++it) {
     // refill the stage released by slab it - 1 with slab it + STAGES - 1 before computing slab it
-    if (threadIdx.x == 0 && it >= 1 && it + STAGES - 1 < nslab) {
+    if (warp == 0 && it >= 1 && it + STAGES - 1 < nslab) {
       const int prev = it - 1;
       mbar_wait(&empty[prev % STAGES], (prev / STAGES) & 1);
       issue(it + STAGES - 1);
