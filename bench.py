@@ -260,6 +260,7 @@ def main():
         return reference_arm(args)
 
     from paper_0804_4809_b200.binding import Handle
+    from paper_0804_4809_b200.sharded import CudaBackend, row_range
 
     world, rank, local = dist_setup(args.gpus)
     cfg, c3t, desc = workload(args.workload)
@@ -270,10 +271,8 @@ def main():
     s, ell = min(m, n), max(m, n)
     if world > 1 and tr:
         raise SystemExit("row sharding applies to the tall (N-branch) configs only")
-    rows = m // world
-    row0 = rank * rows
-    if rank == world - 1:
-        rows = m - row0
+    row0, row1 = row_range(m, world, rank)
+    rows = row1 - row0
     dev = torch.device("cuda", local)
 
     # ---- inputs resident in HBM
@@ -294,20 +293,19 @@ def main():
         e.record(stream)
         return e
 
+    be = CudaBackend(h)
+
     def step(record=False):
+        # the row-sharded step of paper_0804_4809_b200/sharded.py, with events between its stages
         if record:
             p0 = ev()
-        if world > 1:
-            h.geninv_gram_d(G, 0, A)
-            dist.all_reduce(A)                       # a8: A = sum_p G_p'G_p over NVLink
-            p1 = ev() if record else None
-            info = h.geninv_from_gram_d(A)
-        elif tr:
+        if tr:
             info = None
         else:
-            h.geninv_gram_d(G, 0, A)
+            be.gram(G, A)                            # a1 on the local rows
+            be.all_reduce(A)                         # a8: A = sum_p G_p'G_p (NCCL over NVLink; no-op at N = 1)
             p1 = ev() if record else None
-            info = h.geninv_from_gram_d(A)
+            info = be.from_gram(A)                   # a2-a6, replicated
         if tr:                                       # T branch (single GPU): whole call
             _, info = h.geninv_d(G, Gp)
             return info
@@ -315,7 +313,7 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        h.geninv_apply_d(G, 0, Gp)
+        be.apply(G, Gp)                              # a7: local column block of G+
         if record:
             e1.record(stream)
             ev_out.append((e0, e1))

@@ -199,6 +199,27 @@ def geninv(G, tol_rel: float = TOL_REL, tol_abs: float | None = None, keep: bool
     return GeninvResult(Y, ch.rank, tol, transposed, ch, A if keep else None, M if keep else None)
 
 
+def from_gram(A: np.ndarray, tol_rel: float = TOL_REL, tol_abs: float | None = None):
+    """Steps P:117-135 on a given Gram matrix A, plus the left part of the product chain.
+
+    Returns (X, chol) with X = ((L M) M) L' evaluated left to right exactly as the
+    listing's P:139 chain before its final `* G'`, so that geninv(G).Gp == apply(X, G)
+    for the N branch, bit for bit.  Used for the row-sharded split (A = sum_p G_p'G_p).
+    """
+    tol = tolerance(A, tol_rel, tol_abs)
+    ch = full_rank_cholesky(A, tol)
+    if ch.rank == 0:
+        return np.zeros_like(A), ch
+    L = ch.L
+    M = inverse(L.T @ L)
+    return (((L @ M) @ M) @ L.T), ch
+
+
+def apply(X: np.ndarray, G: np.ndarray) -> np.ndarray:
+    """N branch, last product of P:139: Y = X G'."""
+    return X @ G.T
+
+
 def geninv_batched(Gb, tol_rel: float = TOL_REL):
     """geninv applied independently to each matrix of a (batch, m, n) stack.
 

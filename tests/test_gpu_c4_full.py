@@ -1,0 +1,76 @@
+"""C4 at BASELINE.json's full size (2,097,152 x 4096, rank 3584), in the launch configuration bench.py
+times (split C ABI: geninv_gram_d -> geninv_from_gram_d -> geninv_apply_d, one GPU), against the oracle.
+
+The oracle runs on the host from the same G bits (copied device -> host): its Gram is numpy's
+G'G (the listing's `G'*G`), then its own tolerance / full-rank Cholesky / inverse / product
+chain (oracle.from_gram).  Compared: the detected rank and pivot list (exact, inputs in Q),
+X = L M M L' (relative), and sampled columns of G+ = X G' (relative); plus full-size Penrose
+conditions on the GPU with cuBLAS (torch.matmul, a test-only checker independent of the library).
+Needs ~130 GiB of HBM and ~70 GiB of host RAM; takes a few minutes.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import checks as C
+from oracle import geninv_oracle as O
+from paper_0804_4809_b200 import inputs as I
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def test_c4_full_size():
+    from paper_0804_4809_b200.binding import Handle
+    from paper_0804_4809_b200.sharded import CudaBackend, sharded_geninv
+
+    cfg = I.CONFIGS["C4"]
+    m, n = cfg.m, cfg.n
+    h = Handle(0)
+    be = CudaBackend(h)
+    seed = 1
+    G = I.make_single(cfg, seed, device="cuda")
+    A = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+    Gp = torch.empty(n, m, dtype=torch.float64, device="cuda")
+    res = sharded_geninv(be, G, A, Gp)                  # world size 1: the bench's step
+    torch.cuda.synchronize()
+    info = res.info
+    assert info.rank == cfg.rank
+    # device-side pivot list (same A, untimed step entry point)
+    _, piv_gpu, _ = h.geninv_frchol_d(A)
+    piv_gpu = piv_gpu.cpu().numpy()
+    X_gpu = h.geninv_copy_x().cpu().numpy()
+
+    # ---- oracle from the same G bits
+    Gh = G.cpu().numpy()
+    A_or = Gh.T @ Gh                                    # P:114, A = G'G
+    X_or, ch = O.from_gram(A_or)
+    in_q = ch.mu_acc >= 1e4 and ch.mu_drop <= 1e-2
+    print(f"C4 oracle: rank {ch.rank}, mu_acc {ch.mu_acc:.3g}, mu_drop {ch.mu_drop:.3g}, in Q: {in_q}")
+    assert ch.rank == info.rank
+    if in_q:
+        assert np.array_equal(piv_gpu, ch.piv)
+        assert C.rel_fro(X_gpu, X_or) <= 1e-9
+        # sampled columns of G+ (row blocks of G)
+        rng = np.random.default_rng(0)
+        cols = np.sort(rng.choice(m, size=512, replace=False))
+        want = X_or @ Gh[cols].T
+        got = Gp[:, torch.as_tensor(cols, device="cuda")].cpu().numpy()
+        assert C.rel_fro(got, want) <= 1e-9
+    del Gh, A_or
+
+    # ---- full-size Penrose conditions on the GPU (cuBLAS, independent of the library)
+    T = Gp @ G                                          # n x n  (G+ G)
+    rho4 = float(torch.linalg.norm(T.T - T) / torch.linalg.norm(T))
+    e1 = e2 = n1 = n2 = 0.0
+    for c0 in range(0, m, 1 << 18):                     # streamed: no m x n temporaries
+        c1 = min(m, c0 + (1 << 18))
+        e1 += float(torch.linalg.norm(G[c0:c1] @ T - G[c0:c1]) ** 2)         # G G+ G - G
+        n1 += float(torch.linalg.norm(G[c0:c1]) ** 2)
+        e2 += float(torch.linalg.norm(T @ Gp[:, c0:c1] - Gp[:, c0:c1]) ** 2)  # G+ G G+ - G+
+        n2 += float(torch.linalg.norm(Gp[:, c0:c1]) ** 2)
+    rho1, rho2 = (e1 / n1) ** 0.5, (e2 / n2) ** 0.5
+    rows = torch.arange(0, m, m // 8192, device="cuda")[:8192]              # sampled principal block
+    GX = G[rows] @ Gp[:, rows]
+    rho3 = float(torch.linalg.norm(GX.T - GX) / torch.linalg.norm(GX))
+    print("C4 Penrose", rho1, rho2, rho3, rho4)
+    assert max(rho1, rho2, rho3, rho4) <= 1e-10

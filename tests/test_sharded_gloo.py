@@ -1,0 +1,114 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the row-sharded path (`-m "not gpu"`).
+
+paper_0804_4809_b200/sharded.py orchestrates the C4 path: local Gram, one
+all-reduce, replicated factorisation, local column block of G+.  Here the
+arithmetic backend is the oracle (test-only), so the partitioning and the
+exchange are checked on CPU: every rank must see the same A, rank and X, and
+the gathered column blocks must equal the unsharded oracle G+.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_0804_4809_b200 import inputs as I
+from paper_0804_4809_b200.sharded import row_range, sharded_geninv
+
+
+class OracleBackend:
+    def __init__(self):
+        from oracle import geninv_oracle as O
+        self.O = O
+        self.X = None
+
+    def gram(self, G, A):
+        A.copy_(torch.from_numpy(self.O.gram(G.numpy())[0]))
+
+    def all_reduce(self, A):
+        dist.all_reduce(A)
+
+    def from_gram(self, A):
+        X, ch = self.O.from_gram(A.numpy())
+        self.X = X
+        return ch
+
+    def apply(self, G, Gp):
+        Gp.copy_(torch.from_numpy(self.O.apply(self.X, G.numpy())))
+
+    @staticmethod
+    def rank_of(ch):
+        return ch.rank
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, m, n, r, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    G = I.low_rank(21, m, n, r)
+    r0, r1 = row_range(m, world, rank)
+    A = torch.zeros(n, n, dtype=torch.float64)
+    Gp = torch.zeros(n, r1 - r0, dtype=torch.float64)
+    be = OracleBackend()
+    res = sharded_geninv(be, G[r0:r1].contiguous(), A, Gp)
+    # every rank must hold identical A and X bits (the exchange is the only source of A)
+    digest = torch.tensor([float(A.sum()), float(np.abs(be.X).sum()), float(res.rank)], dtype=torch.float64)
+    alld = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(alld, digest)
+    blocks = [None] * world
+    dist.all_gather_object(blocks, (r0, r1, Gp.numpy()))
+    if rank == 0:
+        q.put((res.rank, [d.tolist() for d in alld], blocks))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_matches_unsharded(world):
+    from oracle import checks as C
+    from oracle import geninv_oracle as O
+    m, n, r = 600, 120, 80
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(k, world, port, m, n, r, q)) for k in range(world)]
+    for p in ps:
+        p.start()
+    rank, digests, blocks = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(d == digests[0] for d in digests)        # identical A, X, rank on every rank
+    G = I.low_rank(21, m, n, r).numpy()
+    R = O.geninv(G)
+    assert rank == R.rank == r
+    Gp = np.zeros((n, m))
+    for r0, r1, blk in blocks:
+        Gp[:, r0:r1] = blk
+    assert C.rel_fro(Gp, R.Gp) <= 1e-9
+    assert max(O.penrose_residuals(G, Gp)[0]) <= 1e-10
+
+
+def test_row_range_partition():
+    for m in (7, 600, 1 << 21):
+        for world in (1, 2, 3, 8):
+            rr = [row_range(m, world, k) for k in range(world)]
+            assert rr[0][0] == 0 and rr[-1][1] == m
+            assert all(a[1] == b[0] for a, b in zip(rr, rr[1:]))
+
+
+def test_oracle_split_equals_whole():
+    from oracle import geninv_oracle as O
+    G = I.low_rank(22, 300, 90, 60).numpy()
+    X, ch = O.from_gram(O.gram(G)[0])
+    assert np.array_equal(O.apply(X, G), O.geninv(G).Gp)
