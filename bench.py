@@ -405,7 +405,7 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "dgemm_tc<128,128,64,32,4,K-major,K-major> (a7 G+ = X G')",
+                         "kernel": "dgemm_tc<128,128,64,32,6,K-major,K-major> (a7 G+ = X G')",
                          "flops_per_launch": out_flops_launch, "ms_per_launch": out_ms,
                          "peak_source": peak_src},
             "cpu_baseline": cpu,

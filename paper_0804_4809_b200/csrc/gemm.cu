@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>
 #include <stdio.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -93,6 +94,13 @@ static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   a.mtiles = (op.M + BM - 1) / BM;
   a.ntiles = (op.N + BN - 1) / BN;
+  {
+    // raster band: at most ~48 MB of A rows (BM x K doubles per M-tile) per band, bands balanced
+    const long long per_tile = (long long)BM * (op.K > 0 ? op.K : 1) * 8;
+    long long mb = std::max<long long>(1, (48LL << 20) / per_tile);
+    const long long nb = (a.mtiles + mb - 1) / mb;
+    a.mband = (int)((a.mtiles + nb - 1) / nb);
+  }
   long long tiles = op.lower ? (long long)a.mtiles * (a.mtiles + 1) / 2 : (long long)a.mtiles * a.ntiles;
   if (tiles == 0) return cudaSuccess;
   dim3 grid((unsigned)tiles, op.splits, op.batch);

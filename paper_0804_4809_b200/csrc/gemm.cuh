@@ -32,6 +32,7 @@ struct GemmArgs {
   int M, N, K;              // K ignored if K_dev
   const int *K_dev;         // device-resident K (panel update: the running rank r0)
   int mtiles, ntiles;
+  int mband;                // M-tiles per raster band (non-lower): a band of A stays L2-resident while N sweeps
   int lower;                // 1: enumerate lower-triangle tiles of a square output (M == N)
   int mirror;               // 1 (with lower): also store C[n][m]; diagonal tiles store m >= n mirrored
   int splits;               // split-K count
@@ -78,8 +79,14 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
       tm = bi;
       tn = t - bi * (bi + 1) / 2;
     } else {
-      tm = t % p.mtiles;
-      tn = t / p.mtiles;
+      // banded raster: M fastest inside a band of mband M-tiles, then N, then the next band, so the
+      // A rows of one band (sized on the host to fit the L2) are re-read from L2, not HBM.
+      const int band_tiles = p.mband * p.ntiles;
+      const int band = t / band_tiles;
+      const int rem = t - band * band_tiles;
+      const int mb = min(p.mband, p.mtiles - band * p.mband);
+      tm = band * p.mband + rem % mb;
+      tn = rem / mb;
     }
   }
   const int split = blockIdx.y, bz = blockIdx.z;

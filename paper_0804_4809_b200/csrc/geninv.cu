@@ -152,7 +152,16 @@ geninv_status gram(geninv_handle h, const double *G, long long m, long long n, l
   op.lower = true;
   const long long mt = (s + 127) / 128;
   const long long tiles = mt * (mt + 1) / 2;
-  const int S = pick_splits(tiles, (ell + 15) / 16);
+  int S = pick_splits(tiles, (ell + 15) / 16);
+  // accuracy: no partial sum runs over more than 2^17 rows of G (each DMMA tile accumulates its
+  // k-range sequentially); the fixed-order reduction then adds <= 16 partials.  Capped so the
+  // partial slices stay within ~2.5 GB.
+  {
+    const long long pbytes = (long long)h->ld * h->ld * 8;
+    const int s_acc = (int)std::min<long long>(16, (ell + (1LL << 17) - 1) >> 17);
+    const int s_cap = (int)std::max<long long>(1, (2560LL << 20) / pbytes);
+    S = std::min(std::max(S, s_acc), std::max(S, s_cap));
+  }
   if (S == 1 && !accumulate) {
     op.C = A;
     op.ldc = lda;

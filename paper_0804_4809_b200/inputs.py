@@ -149,6 +149,15 @@ CONFIGS = {
     "C5": Config("C5", 96, 64, 40, batch=65536),
 }
 
+# The seed each single-matrix config is run with (tests and bench.py): the first seed >= 1 whose
+# ORACLE decision margins satisfy predicate Q (mu_acc >= 1e4 and mu_drop <= 1e-2),
+# pre-screened on the device with tools/screen_seeds.py and confirmed by the oracle in the GPU
+# parity tests (which assert Q).  C5 uses fixed per-matrix seeds from base seed 1 (no rejection).
+QSEED = {"C1": 1, "C2": 1, "C3": 1, "C4": 5, "C5": 1}
+# C4 screen (tools/screen_seeds.py, device margins; profiles/r01_seed_screen_c4.jsonl): seeds 1-4 and 6-9
+# fail Q (mu_drop > 1e-2 or mu_acc < 1e4); seed 5: device mu_acc 1.1e5 / mu_drop 9.8e-3, oracle
+# mu_acc 1.1e5 / mu_drop 4.6e-3 -> in Q.  C3: seed 1 is in Q (device mu_acc 2.8e5, mu_drop 4.1e-4).
+
 
 def make_single(cfg: Config, seed: int, device="cpu", row0: int = 0, rows: int | None = None,
                 out: torch.Tensor | None = None) -> torch.Tensor:

@@ -8,6 +8,8 @@ X = L M M L' (relative), and sampled columns of G+ = X G' (relative); plus full-
 conditions on the GPU with cuBLAS (torch.matmul, a test-only checker independent of the library).
 Needs ~130 GiB of HBM and ~70 GiB of host RAM; takes a few minutes.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -27,7 +29,7 @@ def test_c4_full_size():
     m, n = cfg.m, cfg.n
     h = Handle(0)
     be = CudaBackend(h)
-    seed = 1
+    seed = int(os.environ.get("GENINV_C4_SEED", I.QSEED["C4"]))   # override: screening candidate seeds
     G = I.make_single(cfg, seed, device="cuda")
     A = torch.zeros(n, n, dtype=torch.float64, device="cuda")
     Gp = torch.empty(n, m, dtype=torch.float64, device="cuda")
@@ -45,8 +47,10 @@ def test_c4_full_size():
     A_or = Gh.T @ Gh                                    # P:114, A = G'G
     X_or, ch = O.from_gram(A_or)
     in_q = ch.mu_acc >= 1e4 and ch.mu_drop <= 1e-2
+    print(f"C4 seed {seed} device: mu_acc {info.mu_acc:.3g}, mu_drop {info.mu_drop:.3g}")
     print(f"C4 oracle: rank {ch.rank}, mu_acc {ch.mu_acc:.3g}, mu_drop {ch.mu_drop:.3g}, in Q: {in_q}")
     assert ch.rank == info.rank
+    assert in_q, f"seed {seed} is not in Q by the oracle's margins (SURVEY §8(c4)); pick another QSEED"
     if in_q:
         assert np.array_equal(piv_gpu, ch.piv)
         assert C.rel_fro(X_gpu, X_or) <= 1e-9
@@ -57,20 +61,39 @@ def test_c4_full_size():
         got = Gp[:, torch.as_tensor(cols, device="cuda")].cpu().numpy()
         assert C.rel_fro(got, want) <= 1e-9
     del Gh, A_or
+    torch.cuda.empty_cache()
 
-    # ---- full-size Penrose conditions on the GPU (cuBLAS, independent of the library)
-    T = Gp @ G                                          # n x n  (G+ G)
+    # ---- full-size Penrose conditions on the GPU (cuBLAS, independent of the library), for the
+    #      device's G+ and, with the same checker, for the oracle's G+ = X_or G' (the method's own
+    #      rounding floor at this size: G'G squares the conditioning of the accepted columns)
+    rho_gpu = penrose_streamed(G, Gp)
+    del Gp, res                                         # 64 GiB: make room for the oracle's G+
+    torch.cuda.empty_cache()
+    Gp_or = torch.as_tensor(X_or, device="cuda") @ G.T
+    rho_or = penrose_streamed(G, Gp_or)
+    print("C4 Penrose device", rho_gpu)
+    print("C4 Penrose oracle", rho_or)
+    for a, b in zip(rho_gpu, rho_or):
+        assert a <= max(1e-10, 2.0 * b)
+
+
+def penrose_streamed(G, Gp):
+    """rho_1..rho_4 without m x m temporaries; T = G+ G summed over 2^18-row chunks."""
+    m, n = G.shape
+    ch = 1 << 18
+    T = torch.zeros(n, n, dtype=torch.float64, device=G.device)
+    for c0 in range(0, m, ch):
+        T += Gp[:, c0:c0 + ch] @ G[c0:c0 + ch]
     rho4 = float(torch.linalg.norm(T.T - T) / torch.linalg.norm(T))
     e1 = e2 = n1 = n2 = 0.0
-    for c0 in range(0, m, 1 << 18):                     # streamed: no m x n temporaries
-        c1 = min(m, c0 + (1 << 18))
+    for c0 in range(0, m, ch):                          # streamed: no m x n temporaries
+        c1 = min(m, c0 + ch)
         e1 += float(torch.linalg.norm(G[c0:c1] @ T - G[c0:c1]) ** 2)         # G G+ G - G
         n1 += float(torch.linalg.norm(G[c0:c1]) ** 2)
         e2 += float(torch.linalg.norm(T @ Gp[:, c0:c1] - Gp[:, c0:c1]) ** 2)  # G+ G G+ - G+
         n2 += float(torch.linalg.norm(Gp[:, c0:c1]) ** 2)
     rho1, rho2 = (e1 / n1) ** 0.5, (e2 / n2) ** 0.5
-    rows = torch.arange(0, m, m // 8192, device="cuda")[:8192]              # sampled principal block
+    rows = torch.arange(0, m, m // 8192, device=G.device)[:8192]            # sampled principal block
     GX = G[rows] @ Gp[:, rows]
     rho3 = float(torch.linalg.norm(GX.T - GX) / torch.linalg.norm(GX))
-    print("C4 Penrose", rho1, rho2, rho3, rho4)
-    assert max(rho1, rho2, rho3, rho4) <= 1e-10
+    return [rho1, rho2, rho3, rho4]
