@@ -70,6 +70,6 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 
 if __name__ == "__main__":
     if "--timing" in sys.argv:
-        print(build(force=True, defines=("GI_PANEL_TIMING",), out=os.path.join(HERE, "libgeninv_timing.so")))
+        print(build(force=True, defines=("GI_PANEL_TIMING", "GI_BATCHED_TIMING"), out=os.path.join(HERE, "libgeninv_timing.so")))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -20,6 +20,8 @@ from paper_0804_4809_b200.binding import Handle  # noqa: E402
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     cfg = I.CONFIGS["C5"]
+    if len(sys.argv) > 2:                            # smaller batch (profiling)
+        cfg = I.Config("C5", cfg.m, cfg.n, cfg.rank, batch=int(sys.argv[2]))
     h = Handle(0)
     G = I.make_batch(cfg, 1, 0, cfg.batch, device="cuda")
     Gp = torch.empty(cfg.batch, cfg.n, cfg.m, dtype=torch.float64, device="cuda")
