@@ -39,6 +39,11 @@ FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "MEASURED_FP64.json")
 SEED = 1
 
 
+def seed_of(cfg) -> int:
+    """The seed the parity tests use for this config (inputs.QSEED: the oracle's margins are in Q)."""
+    return I.QSEED.get(cfg.name if cfg.name != "C3T" else "C3", SEED)
+
+
 # --------------------------------------------------------------------------- flop model
 def f_alg(s: int, ell: int, piv: np.ndarray) -> dict:
     """Algorithmic FP64 flops of one geninv (SURVEY §8(a) convention: SYRKs count one triangle)."""
@@ -171,9 +176,9 @@ def workload(name: str):
 def make_rows(cfg, transposed_of_c3, row0, rows, device):
     if transposed_of_c3:
         c3 = I.CONFIGS["C3"]
-        G = I.make_single(c3, SEED, device=device)
+        G = I.make_single(c3, seed_of(c3), device=device)
         return G.T[row0:row0 + rows].contiguous()
-    return I.make_single(cfg, SEED, device=device, row0=row0, rows=rows)
+    return I.make_single(cfg, seed_of(cfg), device=device, row0=row0, rows=rows)
 
 
 # --------------------------------------------------------------------------- the reference arm (oracle)
@@ -181,18 +186,18 @@ def oracle_sample(cfg, transposed_of_c3):
     """A bounded sample of the workload for the CPU oracle: its first rows (C4: 16384 of 2^21 rows)."""
     if cfg.name in ("C4",):
         rows = 16384
-        G = I.make_single(cfg, SEED, rows=rows).numpy()
+        G = I.make_single(cfg, seed_of(cfg), rows=rows).numpy()
         return G, f"rows 0..{rows - 1} of the C4 matrix ({rows} x {cfg.n}, same generator, N branch)"
     if transposed_of_c3 or cfg.name == "C3":
         c3 = I.CONFIGS["C3"]
         cols = 4096
-        G = I.make_single(c3, SEED).numpy()
+        G = I.make_single(c3, seed_of(c3)).numpy()
         G = G.T[:cols] if transposed_of_c3 else G[:, :cols].copy()
         return np.ascontiguousarray(G), f"{cols} of 16384 long-side lines of C3"
     if cfg.name == "C5":
-        G = I.make_batch(cfg, SEED, 0, 512).numpy()
+        G = I.make_batch(cfg, seed_of(cfg), 0, 512).numpy()
         return G, "matrices 0..511 of the 65536-matrix batch"
-    G = I.make_single(cfg, SEED).numpy()
+    G = I.make_single(cfg, seed_of(cfg)).numpy()
     return G, "the whole matrix"
 
 
@@ -392,7 +397,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": SEED,
+            "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": seed_of(cfg),
                        "ms_per_matrix": ms, "parallelism": f"rows sharded x{world}" if world > 1 else "single GPU",
                        "pct_fp64_peak": value / (peak * 1e3), "flops_per_step": F["total"],
                        "phase_ms_rank0": phases,
@@ -433,7 +438,7 @@ def e2e_run(args, cfg, c3t, world, rank, local, row0, rows, F, h):
         if c3t:
             blk = make_rows(cfg, c3t, row0 + c0, c1 - c0, dev)
         else:
-            blk = I.make_single(cfg, SEED, device=dev, row0=row0 + c0, rows=c1 - c0)
+            blk = I.make_single(cfg, seed_of(cfg), device=dev, row0=row0 + c0, rows=c1 - c0)
         Gh[c0:c1].copy_(blk)
         del blk
     torch.cuda.synchronize()
@@ -481,7 +486,7 @@ def bench_batched(args, cfg, desc, world, rank):
     dev = torch.device("cuda", local)
     nb = cfg.batch // world
     b0 = rank * nb
-    G = I.make_batch(cfg, SEED, b0, nb, device=dev)
+    G = I.make_batch(cfg, seed_of(cfg), b0, nb, device=dev)
     Gp = torch.empty(nb, cfg.n, cfg.m, dtype=torch.float64, device=dev)
     rk = torch.empty(nb, dtype=torch.int32, device=dev)
     h = Handle(local)

@@ -110,6 +110,18 @@ GENINV_API geninv_status geninv_batched_d(geninv_handle h, const double *G, int6
                                int64_t batch, double *Gp, int64_t ldp, int64_t strideGp, int32_t *rank_dev,
                                const geninv_opts *opts);
 
+/* ---- minimum-norm least-squares solve ---------------------
+ * W = G+ F, the paper's use of G+ for RBF synaptic weights (P:22, P:32-34 with
+ * the "W = G+ W" typo read as W = G+ F, reading R10), without forming
+ * G+: N branch (m >= n) W = X (G' F), T branch (m < n) W = G' (X F), with
+ * X = L M M L' from steps a1-a6.  G: m x n (ld >= n), F: m x k (ldf >= k, even,
+ * 16-byte aligned), W: n x k (ldw >= k), all device, row-major; W is written.
+ * rank / info as for geninv_d.  Synchronises.  The s x k intermediate lives
+ * in the handle's workspace. */
+GENINV_API geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld,
+                             const double *F, int64_t k, int64_t ldf, double *W, int64_t ldw, int64_t *rank,
+                             const geninv_opts *opts, geninv_info *info);
+
 /* ---- split form (row sharding, a8) -----------------------------------------
  * geninv_gram_d: A (s x s, lda >= s, device, caller-owned) = G'G if trans == 0
  *   (s = n), G G' if trans == 1 (s = m).  Lower triangle (and diagonal) written.

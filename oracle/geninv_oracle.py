@@ -215,6 +215,14 @@ def from_gram(A: np.ndarray, tol_rel: float = TOL_REL, tol_abs: float | None = N
     return (((L @ M) @ M) @ L.T), ch
 
 
+def solve(G, F, tol_rel: float = TOL_REL, tol_abs: float | None = None) -> tuple[np.ndarray, int]:
+    """Minimum-norm least-squares weights W = G+ F (P:22, P:32-34 with the garbled "W = G+ W" read as
+    W = G+ F, reading R10; the RBF use of P:96-100): the listing's Y times F.
+    Returns (W (n x k), rank)."""
+    R = geninv(G, tol_rel, tol_abs)
+    return R.Gp @ np.asarray(F, dtype=np.float64), R.rank
+
+
 def apply(X: np.ndarray, G: np.ndarray) -> np.ndarray:
     """N branch, last product of P:139: Y = X G'."""
     return X @ G.T

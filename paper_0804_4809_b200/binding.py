@@ -81,6 +81,9 @@ _SIGS = {
     "geninv_spd_inverse_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                              ctypes.c_int64],
     "geninv_copy_x": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
+    "geninv_solve_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
 }
 
 EXPORTED = sorted(list(_SIGS) + ["geninv_strerror", "geninv_launch_count"])
@@ -190,6 +193,25 @@ class Handle:
         _check(self._lib.geninv_batched_d(self._h, _dev(G, "G"), m, n, G.stride(1), G.stride(0), b, _dev(Gp, "Gp"),
                                           Gp.stride(1), Gp.stride(0), rank.data_ptr(), ctypes.byref(o)))
         return Gp, rank
+
+    def geninv_solve_d(self, G: torch.Tensor, F: torch.Tensor, W: torch.Tensor | None = None, tol_rel=1e-9,
+                       tol_abs=-1.0):
+        """Minimum-norm least-squares W = G+ F (G: m x n, F: m x k) -> (W (n x k), Info)."""
+        m, n = G.shape
+        k = F.shape[1]
+        if F.stride(0) % 2 or F.stride(1) != 1 or F.data_ptr() % 16:   # the TMA view needs an even, aligned ld
+            Fp = torch.zeros(m, (k + 1) // 2 * 2, dtype=torch.float64, device=F.device)
+            Fp[:, :k] = F
+            F = Fp[:, :k]
+        if W is None:
+            W = torch.empty(n, k, dtype=torch.float64, device=G.device)
+        info = _Info()
+        rank = ctypes.c_int64()
+        o = _opts(tol_rel, tol_abs)
+        _check(self._lib.geninv_solve_d(self._h, _dev(G, "G"), m, n, G.stride(0), _dev(F, "F"), k, F.stride(0),
+                                        _dev(W, "W"), W.stride(0), ctypes.byref(rank), ctypes.byref(o),
+                                        ctypes.byref(info)))
+        return W, _info(info)
 
     # ---------------------------------------------------------------- split form
     def geninv_gram_d(self, G: torch.Tensor, trans: int, A: torch.Tensor):

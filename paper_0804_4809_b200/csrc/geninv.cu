@@ -39,6 +39,9 @@ struct geninv_handle_s {
   // host-buffer path staging
   double *Gdev = nullptr, *Gpchunk[2] = {nullptr, nullptr};
   size_t gdev_bytes = 0, chunk_bytes = 0;
+  // least-squares solve (f1): the s x k intermediate G'F or X F
+  double *T1 = nullptr;
+  size_t t1_bytes = 0;
   // state of the last factorisation (for geninv_apply_d)
   int x_s = -1;
   int last_rank = 0;
@@ -177,6 +180,31 @@ geninv_status gram(geninv_handle h, const double *G, long long m, long long n, l
   op.split_stride = pstride;
   GI_TRY(gemm(op, h->st));
   GI_TRY(splitk_reduce(h->part, pstride, S, h->ld, A, lda, accumulate, lda, 1.0, (int)s, (int)s, true, h->st));
+  h->launches += 2;
+  return GENINV_OK;
+}
+
+// One product C (M x N, ldc) = A B with split-K when the output has few tiles (skinny solves:
+// K = m can be millions of rows); partial slices in the handle's Gram workspace, fixed-order sum.
+geninv_status gemm_splitk(geninv_handle h, GemmOp op) {
+  const long long tiles = (long long)((op.M + 127) / 128) * ((op.N + 127) / 128);
+  int S = pick_splits(tiles, (op.K + 15) / 16);
+  const long long pstride = (long long)op.M * op.N;
+  S = (int)std::min<long long>(S, std::max<long long>(1, (1LL << 30) / (pstride * 8)));
+  if (S <= 1) {
+    GI_TRY(gemm(op, h->st));
+    h->launches += 1;
+    return GENINV_OK;
+  }
+  double *C = op.C;
+  const long long ldc = op.ldc;
+  GI_TRYS(ensure_part(h, (size_t)S * pstride * sizeof(double)));
+  op.C = h->part;
+  op.ldc = op.N;
+  op.splits = S;
+  op.split_stride = pstride;
+  GI_TRY(gemm(op, h->st));
+  GI_TRY(splitk_reduce(h->part, pstride, S, op.N, C, ldc, nullptr, 0, 1.0, op.M, op.N, false, h->st));
   h->launches += 2;
   return GENINV_OK;
 }
@@ -385,6 +413,7 @@ geninv_status geninv_destroy(geninv_handle h) {
   free_ws(h);
   if (h->part) cudaFree(h->part);
   if (h->Gdev) cudaFree(h->Gdev);
+  if (h->T1) cudaFree(h->T1);
   for (auto &c : h->Gpchunk)
     if (c) cudaFree(c);
   for (auto &ev : h->ev)
@@ -542,6 +571,75 @@ geninv_status geninv_batched_d(geninv_handle h, const double *G, int64_t m, int6
                         tol_abs_of(opts), h->st));
   h->launches += 1;
   return GENINV_OK;
+}
+
+geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, const double *F,
+                             int64_t k, int64_t ldf, double *W, int64_t ldw, int64_t *rank, const geninv_opts *opts,
+                             geninv_info *info) {
+  if (!h || !F || !W || k < 1 || ldf < k || ldw < k) return GENINV_EINVAL;
+  GI_TRYS(check_g(G, m, n, ld));
+  if (!aligned16(F) || (ldf & 1)) return GENINV_EALIGN;
+  if (k > 0x7fffffffLL) return GENINV_EINVAL;
+  cudaSetDevice(h->device);
+  const int tr = m < n;
+  const int s = (int)(tr ? m : n);
+  GI_TRYS(ensure_ws(h, s));
+  GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
+  int r = 0;
+  FactorStats fs{};
+  geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs);
+  if (st == GENINV_OK) st = finish_spd_check(h, r);
+  if (st != GENINV_OK) {
+    if (rank) *rank = r;
+    fill_info(info, fs, r, tr, st);
+    return st;
+  }
+  const long long ldt = (k + 1) / 2 * 2;
+  const size_t tb = (size_t)s * ldt * sizeof(double);
+  if (tb > h->t1_bytes) {
+    if (h->T1) cudaFree(h->T1);
+    h->T1 = nullptr;
+    h->t1_bytes = 0;
+    GI_TRY(cudaMalloc(&h->T1, tb));
+    h->t1_bytes = tb;
+  }
+  GemmOp a, b;
+  if (!tr) {
+    // T1 (n x k) = G' F:  T1[i][c] = sum_j G[j][i] F[j][c];   W (n x k) = X T1
+    a.A = Mat{G, ld, m, n};
+    a.a_kmajor = false;
+    a.B = Mat{F, ldf, m, k};
+    a.b_kmajor = false;
+    a.M = s; a.N = (int)k; a.K = (int)m;
+    a.C = h->T1; a.ldc = ldt;
+    b.A = Mat{h->X, h->ld, s, s};
+    b.a_kmajor = true;
+    b.B = Mat{h->T1, ldt, s, k};
+    b.b_kmajor = false;
+    b.M = s; b.N = (int)k; b.K = s;
+    b.C = W; b.ldc = ldw;
+  } else {
+    // T1 (m x k) = X F;   W (n x k) = G' T1:  W[i][c] = sum_j G[j][i] T1[j][c]
+    a.A = Mat{h->X, h->ld, s, s};
+    a.a_kmajor = true;
+    a.B = Mat{F, ldf, m, k};
+    a.b_kmajor = false;
+    a.M = s; a.N = (int)k; a.K = s;
+    a.C = h->T1; a.ldc = ldt;
+    b.A = Mat{G, ld, m, n};
+    b.a_kmajor = false;
+    b.B = Mat{h->T1, ldt, s, k};
+    b.b_kmajor = false;
+    b.M = (int)n; b.N = (int)k; b.K = s;
+    b.C = W; b.ldc = ldw;
+  }
+  GI_TRYS(gemm_splitk(h, a));
+  GI_TRYS(gemm_splitk(h, b));
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  if (e != cudaSuccess) st = cuda_status(e);
+  if (rank) *rank = r;
+  fill_info(info, fs, r, tr, st);
+  return st;
 }
 
 geninv_status geninv_gram_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int32_t trans,

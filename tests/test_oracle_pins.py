@@ -56,6 +56,34 @@ def test_golden_min_norm(ex):
     assert np.abs(W - np.array(ex["W"], dtype=float) / ex["den"]).max() <= 1e-12
 
 
+@pytest.mark.parametrize("ex", GOLD["min_norm_solve"], ids=lambda e: e["cite"][:20])
+def test_golden_solve(ex):
+    W, _ = O.solve(np.array(ex["G"], dtype=float), np.array(ex["F"], dtype=float))
+    assert np.abs(W - np.array(ex["W"], dtype=float) / ex["den"]).max() <= 1e-12
+
+
+def test_solve_pins():
+    # full column rank: W is the unique least-squares solution (G'G)^-1 G'F, via QR
+    G = I.dense_normal(21, 300, 40).numpy()
+    F = I.dense_normal(22, 300, 5).numpy()
+    W, r = O.solve(G, F)
+    assert r == 40
+    assert C.rel_fro(W, C.closed_form_full_rank(G) @ F) <= 1e-12
+    # rank deficient, both branches: normal equations G'G W = G'F, and W is orthogonal to null(G)
+    for (m, n) in ((90, 60), (60, 90)):
+        G = I.low_rank(23, m, n, 25).numpy()
+        F = I.dense_normal(24, m, 4).numpy()
+        W, r = O.solve(G, F)
+        assert r == 25
+        lhs, rhs = G.T @ (G @ W), G.T @ F
+        assert np.abs(lhs - rhs).max() <= 1e-8 * np.abs(rhs).max()
+        _, _, Vt = np.linalg.svd(G)
+        Z = Vt[25:].T
+        assert np.abs(Z.T @ W).max() <= 1e-8 * np.abs(W).max()
+        # and equals the brute-force SVD pseudoinverse applied to F
+        assert C.rel_fro(W, C.jacobi_svd_pinv(G, 25) @ F) <= 1e-9
+
+
 @pytest.mark.parametrize("ex", GOLD["svd_pinv"], ids=lambda e: e["cite"][:20])
 def test_golden_svd_checker(ex):
     # the Jacobi checker itself is pinned before it is used to pin the oracle
