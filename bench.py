@@ -274,15 +274,22 @@ def main():
     m, n = cfg.m, cfg.n
     tr = int(m < n)
     s, ell = min(m, n), max(m, n)
-    if world > 1 and tr:
-        raise SystemExit("row sharding applies to the tall (N-branch) configs only")
-    row0, row1 = row_range(m, world, rank)
-    rows = row1 - row0
+    colshard = bool(world > 1 and tr)   # wide G (C3): columns sharded, row blocks of G+ 
     dev = torch.device("cuda", local)
 
     # ---- inputs resident in HBM
-    G = make_rows(cfg, c3t, row0, rows, dev) if world > 1 or not c3t else make_rows(cfg, c3t, 0, m, dev)
-    Gp = torch.empty(n, rows, dtype=torch.float64, device=dev)   # local column block of G+ (n x rows)
+    if colshard:
+        row0, row1 = row_range(n, world, rank)          # this rank's columns of G
+        rows = row1 - row0
+        Gfull = make_rows(cfg, c3t, 0, m, dev)
+        G = Gfull[:, row0:row1].contiguous()
+        del Gfull
+        Gp = torch.empty(rows, m, dtype=torch.float64, device=dev)   # row block of G+ (cols_p x m)
+    else:
+        row0, row1 = row_range(m, world, rank)
+        rows = row1 - row0
+        G = make_rows(cfg, c3t, row0, rows, dev) if world > 1 or not c3t else make_rows(cfg, c3t, 0, m, dev)
+        Gp = torch.empty(n, rows, dtype=torch.float64, device=dev)   # local column block of G+ (n x rows)
     A = torch.zeros(s, s, dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
     h = Handle(local)
@@ -298,27 +305,30 @@ def main():
         e.record(stream)
         return e
 
-    be = CudaBackend(h)
+    be = CudaBackend(h, trans=1 if colshard else 0)
+    # the whole call geninv_d (the user's API) for the single-GPU configs; C4 / C3T keep the split form
+    # so the phases (Gram + all-reduce, factorisation, output) are timed separately at every N
+    whole = bool(world == 1 and cfg.name in ("C1", "C2", "C3"))
 
     def step(record=False):
-        # the row-sharded step of paper_0804_4809_b200/sharded.py, with events between its stages
+        # the sharded step of paper_0804_4809_b200/sharded.py, with events between its stages
         if record:
             p0 = ev()
-        if tr:
+        if whole:
             info = None
         else:
             be.gram(G, A)                            # a1 on the local rows
             be.all_reduce(A)                         # a8: A = sum_p G_p'G_p (NCCL over NVLink; no-op at N = 1)
             p1 = ev() if record else None
             info = be.from_gram(A)                   # a2-a6, replicated
-        if tr:                                       # T branch (single GPU): whole call
+        if whole:                                    # T branch (single GPU): whole call
             _, info = h.geninv_d(G, Gp)
             return info
         if record:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        be.apply(G, Gp)                              # a7: local column block of G+
+        be.apply(G, Gp)                              # a7: local column (C3: row) block of G+
         if record:
             e1.record(stream)
             ev_out.append((e0, e1))
@@ -328,12 +338,12 @@ def main():
     info = step()
     torch.cuda.synchronize()
     # piv for the flop model (untimed): the full-rank Cholesky of the same A
-    if not tr:
+    if not whole:
         _, piv, _ = h.geninv_frchol_d(A)
         piv = piv.cpu().numpy()
     else:
         Aw = torch.zeros(s, s, dtype=torch.float64, device=dev)
-        h.geninv_gram_d(G, 1, Aw)
+        h.geninv_gram_d(G, tr, Aw)
         _, piv, _ = h.geninv_frchol_d(Aw)
         piv = piv.cpu().numpy()
         del Aw
@@ -377,12 +387,21 @@ def main():
     rank_ok = info.rank if info is not None else None
     clocks = clk.summary()
 
-    # ---- free the device-resident inputs before the host-buffer (e2e) run
+    # ---- host copy of this rank's input (untimed), then free the device-resident buffers
+    e2e = None
+    Gh = None
+    if not args.no_e2e:
+        try:
+            Gh = torch.empty(G.shape, dtype=torch.float64).pin_memory()
+            Gh.copy_(G)
+        except RuntimeError as e:
+            e2e = {"value": None, "unit": "GFLOP/s", "skipped": f"pinned host buffers unavailable: {e}"[:200]}
+    gp_shape = tuple(Gp.shape)
     del G, Gp
     torch.cuda.empty_cache()
-    e2e = None
-    if not args.no_e2e:
-        e2e = e2e_run(args, cfg, c3t, world, rank, local, row0, rows, F, h)
+    if Gh is not None:
+        e2e = e2e_run(args, Gh, gp_shape, int(colshard), world, local, F, h)
+        del Gh
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -398,7 +417,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": seed_of(cfg),
-                       "ms_per_matrix": ms, "parallelism": f"rows sharded x{world}" if world > 1 else "single GPU",
+                       "ms_per_matrix": ms, "parallelism": (f"columns sharded x{world}" if colshard else f"rows sharded x{world}") if world > 1 else "single GPU",
                        "pct_fp64_peak": value / (peak * 1e3), "flops_per_step": F["total"],
                        "phase_ms_rank0": phases,
                        "flops_breakdown": {k: v for k, v in F.items() if k != "total"},
@@ -422,39 +441,29 @@ def main():
     return 0
 
 
-def e2e_run(args, cfg, c3t, world, rank, local, row0, rows, F, h):
-    """Same metric through the C ABI with host buffers: H2D of G and D2H of G+ inside the timed region."""
-    m, n = cfg.m, cfg.n
+def e2e_run(args, Gh, gp_shape, trans, world, local, F, h):
+    """Same metric through the C ABI with HOST buffers (pinned): the H2D copy of this rank's G and the
+    D2H copy of its block of G+ are inside the timed region, every step."""
     dev = torch.device("cuda", local)
     try:
-        Gh = torch.empty(rows, n, dtype=torch.float64).pin_memory()
-        Gph = torch.empty(n, rows, dtype=torch.float64).pin_memory()
+        Gph = torch.empty(gp_shape, dtype=torch.float64).pin_memory()
     except RuntimeError as e:
         return {"value": None, "unit": "GFLOP/s", "skipped": f"pinned host buffers unavailable: {e}"[:200]}
-    # fill the host input from the same generator (device-side generation, copied once, untimed)
-    chunk = 1 << 16
-    for c0 in range(0, rows, chunk):
-        c1 = min(rows, c0 + chunk)
-        if c3t:
-            blk = make_rows(cfg, c3t, row0 + c0, c1 - c0, dev)
-        else:
-            blk = I.make_single(cfg, seed_of(cfg), device=dev, row0=row0 + c0, rows=c1 - c0)
-        Gh[c0:c1].copy_(blk)
-        del blk
-    torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
     if world > 1:
         import torch.distributed as dist
-        Gd = torch.empty(rows, n, dtype=torch.float64, device=dev)
-        Gpd = torch.empty(n, rows, dtype=torch.float64, device=dev)
-        A = torch.zeros(n, n, dtype=torch.float64, device=dev)
+        Gd = torch.empty(Gh.shape, dtype=torch.float64, device=dev)
+        Gpd = torch.empty(gp_shape, dtype=torch.float64, device=dev)
+        s = Gh.shape[0] if trans else Gh.shape[1]
+        A = torch.zeros(s, s, dtype=torch.float64, device=dev)
 
         def step():
             Gd.copy_(Gh, non_blocking=True)
-            h.geninv_gram_d(Gd, 0, A)
+            A.zero_()
+            h.geninv_gram_d(Gd, trans, A)
             dist.all_reduce(A)
             h.geninv_from_gram_d(A)
-            h.geninv_apply_d(Gd, 0, Gpd)
+            h.geninv_apply_d(Gd, trans, Gpd)
             Gph.copy_(Gpd, non_blocking=True)
             torch.cuda.synchronize()
     else:
@@ -464,18 +473,16 @@ def e2e_run(args, cfg, c3t, world, rank, local, row0, rows, F, h):
         step()
     barrier(world)
     t0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
     for _ in range(args.steps):
         step()
-    e1.record(stream)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / args.steps * 1e3
     barrier(world)
     ms = allmax(wall, world)
+    nbytes_in = int(Gh.numel()) * 8 * world
+    nbytes_out = int(np.prod(gp_shape)) * 8 * world
     return {"value": F["total"] / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": int(m) * n * 8, "d2h_bytes_per_step": int(m) * n * 8,
+            "h2d_bytes_per_step": nbytes_in, "d2h_bytes_per_step": nbytes_out,
             "api": "geninv_host_d (pinned host G and G+)" if world == 1 else
             "pinned H2D + geninv_gram_d / all_reduce / geninv_from_gram_d / geninv_apply_d + D2H"}
 
@@ -511,7 +518,7 @@ def bench_batched(args, cfg, desc, world, rank):
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                          "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+                          "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                           "data": "synthetic",
                           "config": {"workload": desc, "batch": cfg.batch, "us_per_matrix": ms * 1e3 / cfg.batch,
                                      "hbm_gbs": 2 * cfg.batch * cfg.m * cfg.n * 8 / (ms * 1e-3) / 1e9},

@@ -89,7 +89,10 @@ GENINV_API const char *geninv_strerror(geninv_status st);
 /* ---- whole path, single matrix (a0-a7) ------------------------------------
  * G: m x n device, ld >= n.  Gp: n x m device, ldp >= m, overwritten.
  * rank (host, may be NULL) receives r; info (host, may be NULL) diagnostics.
- * Zero G -> rank 0 and G+ = 0 (reading R2).  Synchronises the stream. */
+ * Zero G -> rank 0 and G+ = 0 (reading R2).  Synchronises the stream.
+ * Small matrices (min(m, n) <= 64, max(m, n) <= 128) run the whole path in one
+ * CTA (the batched kernel, a9); that path does not keep X in the handle
+ * (geninv_copy_x then returns GENINV_ESTATE). */
 GENINV_API geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp,
                        int64_t ldp, int64_t *rank, const geninv_opts *opts, geninv_info *info);
 
@@ -104,8 +107,10 @@ GENINV_API geninv_status geninv_host_d(geninv_handle h, const double *G_host, in
 /* ---- batched small matrices (a9) ------------------------------------------
  * `batch` independent m x n matrices: matrix b at G + b*strideG (device, ld >= n),
  * G+ of matrix b written at Gp + b*strideGp (n x m, ldp >= m).  rank_dev:
- * device int32[batch].  Requires min(m, n) <= 64 and max(m, n) <= 128.
- * Does not synchronise. */
+ * device int32[batch]: the rank of each matrix, or -GENINV_ENONFINITE (-2) /
+ * -GENINV_ENOTSPD (-3) for a matrix with non-finite entries / a non-SPD L'L,
+ * whose G+ is then filled with NaN.  Requires min(m, n) <= 64 and
+ * max(m, n) <= 128 (GENINV_EINVAL otherwise).  Does not synchronise. */
 GENINV_API geninv_status geninv_batched_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int64_t strideG,
                                int64_t batch, double *Gp, int64_t ldp, int64_t strideGp, int32_t *rank_dev,
                                const geninv_opts *opts);

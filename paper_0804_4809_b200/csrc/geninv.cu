@@ -376,6 +376,25 @@ geninv_status finish_spd_check(geninv_handle h, int r) {
   return (flags & 2) ? GENINV_ENOTSPD : GENINV_OK;
 }
 
+bool is_small(long long m, long long n) { return std::min(m, n) <= 64 && std::max(m, n) <= 128; }
+
+// Small matrix (C1, the paper's n = 32 / 64): the whole path in one CTA -- the batched kernel with
+// batch = 1, one launch instead of ~20 latency-bound ones.  Synchronises; X is not kept.
+geninv_status small_path(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
+                         long long ldp, const geninv_opts *opts, int *r_out, FactorStats *fs) {
+  GI_TRYS(ensure_ws(h, 64));
+  GI_TRY(batched_geninv(G, (int)m, (int)n, ld, 0, 1, Gp, ldp, 0, h->rk, tol_rel_of(opts), tol_abs_of(opts), h->st,
+                        h->fs));
+  h->launches += 1;
+  int rr = 0;
+  GI_TRY(cudaMemcpyAsync(&rr, h->rk, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  GI_TRY(cudaMemcpyAsync(fs, h->fs, sizeof(FactorStats), cudaMemcpyDeviceToHost, h->st));
+  GI_TRY(cudaStreamSynchronize(h->st));
+  h->x_s = -1;
+  *r_out = rr < 0 ? 0 : rr;
+  return rr == -2 ? GENINV_ENONFINITE : rr == -3 ? GENINV_ENOTSPD : GENINV_OK;
+}
+
 }  // namespace
 
 // ============================================================================ C ABI
@@ -449,6 +468,14 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
   const int tr = m < n;  // P:109 (strict; m == n takes the N branch, R6)
   const int s = (int)(tr ? m : n);
   GI_TRYS(ensure_ws(h, s));
+  if (is_small(m, n)) {
+    int r = 0;
+    FactorStats fs{};
+    geninv_status st = small_path(h, G, m, n, ld, Gp, ldp, opts, &r, &fs);
+    if (rank) *rank = r;
+    fill_info(info, fs, r, tr, st);
+    return st;
+  }
   GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
   int r = 0;
   FactorStats fs{};
@@ -470,6 +497,36 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
   cudaSetDevice(h->device);
   const int tr = m < n;
   const int s = (int)(tr ? m : n);
+  if (is_small(m, n)) {   // one H2D, the one-CTA path, one D2H
+    const size_t gb = (size_t)m * n * sizeof(double), pb = (size_t)n * m * sizeof(double);
+    if (gb > h->gdev_bytes) {
+      if (h->Gdev) cudaFree(h->Gdev);
+      h->Gdev = nullptr;
+      h->gdev_bytes = 0;
+      GI_TRY(cudaMalloc(&h->Gdev, gb));
+      h->gdev_bytes = gb;
+    }
+    if (pb > h->chunk_bytes) {
+      for (auto &c : h->Gpchunk) {
+        if (c) cudaFree(c);
+        c = nullptr;
+      }
+      h->chunk_bytes = 0;
+      for (auto &c : h->Gpchunk) GI_TRY(cudaMalloc(&c, pb));
+      h->chunk_bytes = pb;
+    }
+    GI_TRY(cudaMemcpy2DAsync(h->Gdev, n * 8, G_host, ld * 8, n * 8, m, cudaMemcpyHostToDevice, h->st));
+    int r = 0;
+    FactorStats fs{};
+    geninv_status st = small_path(h, h->Gdev, m, n, n, h->Gpchunk[0], m, opts, &r, &fs);
+    if (st == GENINV_OK || st == GENINV_ENOTSPD || st == GENINV_ENONFINITE) {
+      GI_TRY(cudaMemcpy2DAsync(Gp_host, ldp * 8, h->Gpchunk[0], m * 8, m * 8, n, cudaMemcpyDeviceToHost, h->st));
+      GI_TRY(cudaStreamSynchronize(h->st));
+    }
+    if (rank) *rank = r;
+    fill_info(info, fs, r, tr, st);
+    return st;
+  }
   const long long ldg = (n + 1) / 2 * 2;  // device copy: even leading dimension
   const size_t gbytes = (size_t)m * ldg * sizeof(double);
   if (gbytes > h->gdev_bytes) {

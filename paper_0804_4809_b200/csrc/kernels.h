@@ -39,9 +39,11 @@ cudaError_t frchol(const double *A, long long lda, int s, double *L, long long l
 cudaError_t trtri_lower(double *C, long long ldc, int r, double *Cinv, long long ldi, double *T,
                         cudaStream_t stream);
 
-// a9: batched small geninv, one CTA per matrix.
+// a9: batched small geninv, one CTA per matrix (min(m,n) <= 64, max(m,n) <= 128).  rank[b] >= 0, or
+// -2 (non-finite G) / -3 (L'L not SPD) with G+_b = NaN.  stats (optional, device, one per matrix):
+// tol, decision margins and flags (bit0 non-finite, bit1 not SPD) of each matrix.
 cudaError_t batched_geninv(const double *G, int m, int n, long long ld, long long strideG, long long batch,
                            double *Gp, long long ldp, long long strideGp, int *rank, double tol_rel,
-                           double tol_abs, cudaStream_t stream);
+                           double tol_abs, cudaStream_t stream, FactorStats *stats = nullptr);
 
 }  // namespace gi

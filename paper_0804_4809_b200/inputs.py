@@ -211,6 +211,16 @@ def make_batch(cfg: Config, base_seed: int, b0: int = 0, count: int | None = Non
     return out
 
 
+# Seed used for the paper's family at each n (the first seed >= 1 whose ORACLE margins are in Q,
+# as for the configs; asserted by tests/test_gpu_paper_family.py).  Seed 1 misses Q at n = 128
+# (mu_drop 0.013) and n = 1024 (mu_drop 0.048), where even the oracle's G+ exceeds the paper's
+# 2e-10 per-coefficient bound.
+PAPER_QSEED = {32: 1, 64: 1, 128: 2, 256: 1, 512: 1, 1024: 2, 2048: 1, 4096: 1, 8192: 1}
+# ... and the first seed whose oracle margins are in Q* (mu_acc >= 1e6, mu_drop <= 1e-3): the inputs on
+# which the paper's 2e-10 per-coefficient statement is checked (reading R22).
+PAPER_QSTAR_SEED = {32: 1, 64: 2, 128: 3, 256: 1, 512: 9, 1024: 17}
+
+
 def paper_family(n: int, seed: int, device="cpu") -> torch.Tensor:
     """The paper's own test family: m = 2n, rank r = 7n/8, coefficients in [-1, 1].
 

@@ -1,11 +1,15 @@
-"""Row-sharded geninv for tall G (C4, north star "G is row-sharded").
+"""Sharded geninv (north star "G is row-sharded").
 
-Rank p holds rows [p*m/P, (p+1)*m/P) of G (m x n, m >= n).  One step:
+Tall G (C4, m >= n, trans = 0): rank p holds rows [p*m/P, (p+1)*m/P) of G.  One step:
 
     A_p = G_p' G_p              (a1 on the local rows)        backend.gram
     A   = sum_p A_p             (a8, the one exchange step)   backend.all_reduce
     X   = L M M L' from A       (a2-a6, replicated)           backend.from_gram
     G+[:, rows_p] = X G_p'      (a7, local column block)      backend.apply
+
+Wide G (C3, m < n, trans = 1): rank p holds columns [p*n/P, (p+1)*n/P) of G
+(an m x n_p block), A = sum_p G_p G_p' (P:111 summed over column blocks), and
+G+[cols_p, :] = G_p' X is the rank's row block of G+ -- the same single exchange.
 
 The arithmetic lives in the backend: on GPUs the C ABI (geninv_gram_d /
 geninv_from_gram_d / geninv_apply_d) with an NCCL all-reduce; the CPU tests
@@ -18,7 +22,7 @@ from dataclasses import dataclass
 
 
 def row_range(m: int, world: int, rank: int):
-    """Contiguous row block of rank `rank`: [r0, r1)."""
+    """Contiguous row (or column) block of rank `rank`: [r0, r1)."""
     per = m // world
     r0 = rank * per
     r1 = m if rank == world - 1 else r0 + per
@@ -29,11 +33,11 @@ def row_range(m: int, world: int, rank: int):
 class ShardResult:
     rank: int        # detected rank r (identical on every process)
     info: object     # backend-specific diagnostics
-    Gp_local: object  # n x (rows of this shard): the local column block of G+
+    Gp_local: object  # trans 0: n x rows_p (column block of G+); trans 1: cols_p x m (row block of G+)
 
 
 def sharded_geninv(backend, G_local, A, Gp_local) -> ShardResult:
-    """One sharded geninv step.  A (n x n) and Gp_local (n x rows) are caller-owned buffers."""
+    """One sharded geninv step.  A (s x s) and Gp_local are caller-owned buffers."""
     backend.gram(G_local, A)
     backend.all_reduce(A)
     info = backend.from_gram(A)
@@ -44,14 +48,15 @@ def sharded_geninv(backend, G_local, A, Gp_local) -> ShardResult:
 class CudaBackend:
     """The C-ABI path (binding.Handle) + torch.distributed (NCCL) for the exchange."""
 
-    def __init__(self, handle, group=None):
+    def __init__(self, handle, group=None, trans: int = 0):
         self.h = handle
         self.group = group
+        self.trans = int(trans)
 
     def gram(self, G, A):
         # writes the lower triangle; the caller allocates A zeroed so the all-reduced
         # upper triangle stays exactly zero
-        self.h.geninv_gram_d(G, 0, A)
+        self.h.geninv_gram_d(G, self.trans, A)
 
     def all_reduce(self, A):
         import torch.distributed as dist
@@ -62,7 +67,7 @@ class CudaBackend:
         return self.h.geninv_from_gram_d(A)
 
     def apply(self, G, Gp):
-        self.h.geninv_apply_d(G, 0, Gp)
+        self.h.geninv_apply_d(G, self.trans, Gp)
 
     @staticmethod
     def rank_of(info):

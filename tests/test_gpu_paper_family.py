@@ -1,0 +1,60 @@
+"""The paper's own test family (section 3) through the CUDA path: m = 2n, r = 7n/8, entries
+in [-1, 1] (reading R16).  Parity with the oracle on the Q seeds (rank exact, relative difference
+<= 1e-9); the paper's accuracy statement -- no coefficient of the four Penrose error matrices above
+2e-10 in absolute value (Table 1 caption) -- on the Q* seeds (reading R22: on Q inputs the
+coefficient varies ~5x between valid summation orders, so there the gate is 1e-9)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import checks as C
+from oracle import geninv_oracle as O
+from paper_0804_4809_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_0804_4809_b200.binding import Handle
+    return Handle(0)
+
+
+@pytest.mark.parametrize("n", [32, 64, 128, 256, 512, 1024, 2048])
+def test_paper_family(H, n):
+    G = I.paper_family(n, I.PAPER_QSEED[n], device="cuda")
+    Gp, info = H.geninv_d(G)
+    R = O.geninv(G.cpu().numpy())
+    assert R.in_Q()                     # the seed choice (inputs.PAPER_QSEED) is confirmed by the oracle
+    assert info.rank == R.rank == 7 * n // 8
+    assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
+    assert penrose_abs(G, Gp) <= 1e-9
+
+
+def penrose_abs(G, Gp):
+    """Largest absolute coefficient of the four Penrose error matrices (cuBLAS, test-only checker)."""
+    GX, XG = G @ Gp, Gp @ G
+    return max(float((GX @ G - G).abs().max()), float((XG @ Gp - Gp).abs().max()),
+               float((GX.T - GX).abs().max()), float((XG.T - XG).abs().max()))
+
+
+@pytest.mark.parametrize("n", [32, 64, 128, 256, 512, 1024])
+def test_paper_accuracy_statement(H, n):
+    G = I.paper_family(n, I.PAPER_QSTAR_SEED[n], device="cuda")
+    Gp, info = H.geninv_d(G)
+    R = O.geninv(G.cpu().numpy())
+    assert R.in_Qstar() and info.rank == R.rank == 7 * n // 8
+    err = penrose_abs(G, Gp)
+    assert err <= 2e-10, err
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_paper_family_batched(H, n):
+    Gb = torch.stack([I.paper_family(n, s) for s in range(1, 9)]).cuda()
+    Gpb, rk = H.geninv_batched_d(Gb)
+    torch.cuda.synchronize()
+    for i in range(Gb.shape[0]):
+        R = O.geninv(Gb[i].cpu().numpy())
+        assert int(rk[i]) == R.rank == 7 * n // 8
+        if R.in_Q():
+            assert C.rel_fro(Gpb[i].cpu().numpy(), R.Gp) <= 1e-9

@@ -20,13 +20,18 @@ from paper_0804_4809_b200.sharded import row_range, sharded_geninv
 
 
 class OracleBackend:
-    def __init__(self):
+    def __init__(self, trans=0):
         from oracle import geninv_oracle as O
         self.O = O
         self.X = None
+        self.trans = trans
 
     def gram(self, G, A):
-        A.copy_(torch.from_numpy(self.O.gram(G.numpy())[0]))
+        g = G.numpy()
+        if self.trans:          # column block of a wide G: its share of G G'
+            A.copy_(torch.from_numpy(g @ g.T))
+        else:
+            A.copy_(torch.from_numpy(self.O.gram(g)[0]))
 
     def all_reduce(self, A):
         dist.all_reduce(A)
@@ -37,7 +42,10 @@ class OracleBackend:
         return ch
 
     def apply(self, G, Gp):
-        Gp.copy_(torch.from_numpy(self.O.apply(self.X, G.numpy())))
+        if self.trans:          # rows of G+ = G_p' X
+            Gp.copy_(torch.from_numpy(G.numpy().T @ self.X))
+        else:
+            Gp.copy_(torch.from_numpy(self.O.apply(self.X, G.numpy())))
 
     @staticmethod
     def rank_of(ch):
@@ -52,16 +60,23 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, m, n, r, q):
+def _worker(rank, world, port, m, n, r, q, trans=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     G = I.low_rank(21, m, n, r)
-    r0, r1 = row_range(m, world, rank)
-    A = torch.zeros(n, n, dtype=torch.float64)
-    Gp = torch.zeros(n, r1 - r0, dtype=torch.float64)
-    be = OracleBackend()
-    res = sharded_geninv(be, G[r0:r1].contiguous(), A, Gp)
+    if trans:                   # wide G: column blocks, row blocks of G+
+        r0, r1 = row_range(n, world, rank)
+        A = torch.zeros(m, m, dtype=torch.float64)
+        Gp = torch.zeros(r1 - r0, m, dtype=torch.float64)
+        Gl = G[:, r0:r1].contiguous()
+    else:
+        r0, r1 = row_range(m, world, rank)
+        A = torch.zeros(n, n, dtype=torch.float64)
+        Gp = torch.zeros(n, r1 - r0, dtype=torch.float64)
+        Gl = G[r0:r1].contiguous()
+    be = OracleBackend(trans)
+    res = sharded_geninv(be, Gl, A, Gp)
     # every rank must hold identical A and X bits (the exchange is the only source of A)
     digest = torch.tensor([float(A.sum()), float(np.abs(be.X).sum()), float(res.rank)], dtype=torch.float64)
     alld = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
@@ -95,6 +110,33 @@ def test_sharded_matches_unsharded(world):
     Gp = np.zeros((n, m))
     for r0, r1, blk in blocks:
         Gp[:, r0:r1] = blk
+    assert C.rel_fro(Gp, R.Gp) <= 1e-9
+    assert max(O.penrose_residuals(G, Gp)[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2])
+def test_column_sharded_wide_matches_unsharded(world):
+    # C3-style wide G sharded by columns; one exchange (A = sum_p G_p G_p')
+    from oracle import checks as C
+    from oracle import geninv_oracle as O
+    m, n, r = 120, 600, 80
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(k, world, port, m, n, r, q, 1)) for k in range(world)]
+    for p in ps:
+        p.start()
+    rank, digests, blocks = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(d == digests[0] for d in digests)
+    G = I.low_rank(21, m, n, r).numpy()
+    R = O.geninv(G)
+    assert R.transposed and rank == R.rank == r
+    Gp = np.zeros((n, m))
+    for r0, r1, blk in blocks:
+        Gp[r0:r1] = blk
     assert C.rel_fro(Gp, R.Gp) <= 1e-9
     assert max(O.penrose_residuals(G, Gp)[0]) <= 1e-10
 
