@@ -219,3 +219,38 @@ def test_c1_batched_matches_single(H):
         R = O.geninv(G2[i].cpu().numpy())
         assert int(r2[i]) == R.rank == 17
         assert C.rel_fro(Gp2[i].cpu().numpy(), R.Gp) <= REL
+
+
+def test_batched_error_codes(H):
+    # a batch with one non-finite matrix: its rank is -GENINV_ENONFINITE (-2) and its G+ is NaN; the
+    # other matrices are unaffected (header: geninv_batched_d)
+    cfg = I.CONFIGS["C1"]
+    Gs = torch.stack([I.make_single(cfg, s) for s in (1, 2, 3)]).cuda()
+    Gs[1, 5, 7] = float("nan")
+    Gp, rank = H.geninv_batched_d(Gs)
+    torch.cuda.synchronize()
+    assert int(rank[1]) == -2 and torch.isnan(Gp[1]).all()
+    for i in (0, 2):
+        R = O.geninv(Gs[i].cpu().numpy())
+        assert int(rank[i]) == R.rank
+        assert C.rel_fro(Gp[i].cpu().numpy(), R.Gp) <= REL
+
+
+def test_small_path_info_matches_oracle(H):
+    # small single matrices run the one-CTA kernel inside geninv_d; its diagnostics must agree with the
+    # oracle's own decision margins (tol exactly the same formula; mu's to rounding)
+    for (m, n, r) in ((64, 48, 32), (40, 90, 17), (128, 64, 64)):
+        G = I.low_rank(m + n, m, n, r).numpy()
+        R = O.geninv(G)
+        Gp, info = run(H, G)
+        assert info.rank == R.rank and info.transposed == (m < n)
+        assert info.tol == pytest.approx(R.tol, rel=1e-12)
+        if R.in_Q():
+            assert info.mu_acc == pytest.approx(R.chol.mu_acc, rel=1e-3)
+            assert C.rel_fro(Gp, R.Gp) <= REL
+    # host buffers take the same path
+    G = I.low_rank(7, 64, 48, 32).numpy()
+    Gh = torch.as_tensor(G).pin_memory()
+    Gph = torch.empty(48, 64, dtype=torch.float64).pin_memory()
+    _, info = H.geninv_host_d(Gh, Gph)
+    assert C.rel_fro(Gph.numpy(), O.geninv(G).Gp) <= REL
