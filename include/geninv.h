@@ -74,6 +74,9 @@ typedef struct {
   double min_acc;    /* smallest accepted pivot c_k (before sqrt); +inf if none */
   double max_drop;   /* largest |c_k| over dropped columns; 0 if none */
   double min_pivot;  /* smallest c_k over all columns */
+  int32_t order;     /* a7 product order used by geninv_d: 0 = X G' / G' X with X = K K';
+                        1 = K (K' G') / (G' K) K' (low rank) */
+  int32_t reserved;
 } geninv_info;
 
 typedef struct geninv_handle_s *geninv_handle;
@@ -92,7 +95,10 @@ GENINV_API const char *geninv_strerror(geninv_status st);
  * Zero G -> rank 0 and G+ = 0 (reading R2).  Synchronises the stream.
  * Small matrices (min(m, n) <= 64, max(m, n) <= 128) run the whole path in one
  * CTA (the batched kernel, a9); that path does not keep X in the handle
- * (geninv_copy_x then returns GENINV_ESTATE). */
+ * (geninv_copy_x then returns GENINV_ESTATE).  For low rank, where
+ * 4 r s l < s (s + 1) r + 2 s^2 l (s = min(m, n), l = max(m, n)), geninv_d skips
+ * X and evaluates G+ = K (K' G') (m >= n) or (G' K) K' (m < n) with K = L M,
+ * in chunks of the long side (info->order = 1; X is then not kept either). */
 GENINV_API geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp,
                        int64_t ldp, int64_t *rank, const geninv_opts *opts, geninv_info *info);
 

@@ -35,7 +35,7 @@ class _Opts(ctypes.Structure):
 class _Info(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("rank", ctypes.c_int64), ("transposed", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("min_acc", ctypes.c_double), ("max_drop", ctypes.c_double),
-                ("min_pivot", ctypes.c_double)]
+                ("min_pivot", ctypes.c_double), ("order", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 @dataclass
@@ -47,6 +47,7 @@ class Info:
     min_acc: float
     max_drop: float
     min_pivot: float
+    order: int = 0       # a7 product order of geninv_d: 0 = X G', 1 = K (K' G') (low rank, f4)
 
     @property
     def mu_acc(self):
@@ -268,4 +269,5 @@ class Handle:
 
 
 def _info(i: _Info) -> Info:
-    return Info(i.tol, int(i.rank), bool(i.transposed), int(i.status), i.min_acc, i.max_drop, i.min_pivot)
+    return Info(i.tol, int(i.rank), bool(i.transposed), int(i.status), i.min_acc, i.max_drop, i.min_pivot,
+                int(i.order))

@@ -257,8 +257,8 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   return GENINV_OK;
 }
 
-// a4-a6 after the factorisation: X (s x s, full) = L M M L'.
-geninv_status build_x(geninv_handle h, int s, int r) {
+// a4-a6 after the factorisation: K = L M (s x r) and, if want_x, X (s x s, full) = K K' = L M M L'.
+geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true) {
   const long long ld = h->ld;
   if (r == 0) {
     GI_TRY(cudaMemsetAsync(h->X, 0, (size_t)s * ld * sizeof(double), h->st));
@@ -290,6 +290,8 @@ geninv_status build_x(geninv_handle h, int s, int r) {
   k.C = h->Kb;
   k.ldc = ld;
   GI_TRY(gemm(k, h->st));
+  h->launches += 1;
+  if (!want_x) return GENINV_OK;
   // X = K K' (s x s, full symmetric)
   GemmOp x;
   x.A = Mat{h->Kb, ld, s, r};
@@ -302,7 +304,59 @@ geninv_status build_x(geninv_handle h, int s, int r) {
   x.C = h->X;
   x.ldc = ld;
   GI_TRY(gemm(x, h->st));
-  h->launches += 2;
+  h->launches += 1;
+  return GENINV_OK;
+}
+
+// Order switch: G+ = K (K' G') / (G' K) K' costs 4 r s ell flops against
+// s(s+1) r + 2 s^2 ell for X = K K' then X G'; the K order wins for low rank (roughly r < s/2).
+bool k_order_cheaper(long long s, long long ell, long long r) {
+  return r > 0 && 4.0 * r * s * ell < (double)s * (s + 1) * r + 2.0 * s * s * ell;
+}
+
+// a7 in the K order, in chunks of the long side through the handle's s x s scratch T:
+//   N: T (r x c) = K' G[j0:j0+c]',  G+[:, j0:j0+c] = K T;   T: T (c x r) = G[:, i0:i0+c]' K,  G+[i0:i0+c, :] = T K'
+geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans,
+                      double *Gp, long long ldp, int r) {
+  const long long s = trans ? m : n, ell = trans ? n : m;
+  const long long cap = (long long)h->ld * h->ld;
+  const int rp = (r + 1) / 2 * 2;
+  const long long c = std::min<long long>((ell + 1) / 2 * 2, std::max<long long>(128, cap / rp / 128 * 128));
+  for (long long c0 = 0; c0 < ell; c0 += c) {
+    const long long w = std::min(c, ell - c0);   // c even: the T view has an even leading dimension
+    GemmOp a, b;
+    if (!trans) {
+      a.A = Mat{h->Kb, h->ld, s, r};       // A(q, i) = K[i][q]  (MN-major)
+      a.a_kmajor = false;
+      a.B = Mat{G + c0 * ld, ld, w, n};    // B(i, j) = G[c0 + j][i]  (K-major)
+      a.b_kmajor = true;
+      a.M = r; a.N = (int)w; a.K = (int)s;
+      a.C = h->T; a.ldc = c;
+      b.A = Mat{h->Kb, h->ld, s, r};       // A(i, q) = K[i][q]
+      b.a_kmajor = true;
+      b.B = Mat{h->T, c, r, c};            // B(q, j) = T[q][j]  (MN-major)
+      b.b_kmajor = false;
+      b.M = (int)s; b.N = (int)w; b.K = r;
+      b.C = Gp + c0; b.ldc = ldp;
+    } else {
+      a.A = Mat{G, ld, m, n};              // A(i, j) = G[j][c0 + i]  (MN-major)
+      a.a_kmajor = false;
+      a.a_mn0 = (int)c0;
+      a.B = Mat{h->Kb, h->ld, s, r};       // B(j, q) = K[j][q]  (MN-major)
+      a.b_kmajor = false;
+      a.M = (int)w; a.N = r; a.K = (int)s;
+      a.C = h->T; a.ldc = rp;
+      b.A = Mat{h->T, rp, w, r};           // A(i, q) = T[i][q]
+      b.a_kmajor = true;
+      b.B = Mat{h->Kb, h->ld, s, r};       // B(q, j) = K[j][q]  (K-major)
+      b.b_kmajor = true;
+      b.M = (int)w; b.N = (int)s; b.K = r;
+      b.C = Gp + c0 * ldp; b.ldc = ldp;
+    }
+    GI_TRY(gemm(a, h->st));
+    GI_TRY(gemm(b, h->st));
+    h->launches += 2;
+  }
   return GENINV_OK;
 }
 
@@ -345,6 +399,7 @@ void fill_info(geninv_info *info, const FactorStats &fs, int r, int tr, geninv_s
   info->min_acc = fs.min_acc;
   info->max_drop = fs.max_drop;
   info->min_pivot = fs.min_pivot;
+  info->order = 0;
 }
 
 geninv_status check_g(const double *G, long long m, long long n, long long ld) {
@@ -354,15 +409,18 @@ geninv_status check_g(const double *G, long long m, long long n, long long ld) {
   return GENINV_OK;
 }
 
-// Steps a2-a6 on A (s x s lower, lda); leaves X in the handle.
+// Steps a2-a6 on A (s x s lower, lda); leaves X in the handle -- or, when ell > 0 and the K order
+// is cheaper for this rank (f4), only K (*k_order = true, X not formed).
 geninv_status from_gram(geninv_handle h, const double *A, int s, long long lda, const geninv_opts *opts, int *r_out,
-                        FactorStats *fs) {
+                        FactorStats *fs, long long ell = 0, bool *k_order = nullptr) {
   GI_TRYS(ensure_ws(h, s));
   int r = 0;
   geninv_status st = factor(h, A, lda, s, h->L, h->ld, h->piv, opts, &r, fs);
   if (st != GENINV_OK) return st;
-  GI_TRYS(build_x(h, s, r));
-  h->x_s = s;
+  const bool ko = ell > 0 && k_order && k_order_cheaper(s, ell, r);
+  if (k_order) *k_order = ko;
+  GI_TRYS(build_x(h, s, r, !ko));
+  h->x_s = ko ? -1 : s;
   h->last_rank = r;
   *r_out = r;
   return GENINV_OK;
@@ -479,8 +537,9 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
   GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
   int r = 0;
   FactorStats fs{};
-  geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs);
-  if (st == GENINV_OK) st = apply(h, G, m, n, ld, tr, Gp, ldp, h->st);
+  bool ko = false;
+  geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs, tr ? n : m, &ko);
+  if (st == GENINV_OK) st = ko ? apply_k(h, G, m, n, ld, tr, Gp, ldp, r) : apply(h, G, m, n, ld, tr, Gp, ldp, h->st);
   if (st == GENINV_OK) st = finish_spd_check(h, r);
   if (st == GENINV_OK) {
     cudaError_t e = cudaStreamSynchronize(h->st);
@@ -488,6 +547,7 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
   }
   if (rank) *rank = r;
   fill_info(info, fs, r, tr, st);
+  if (info) info->order = ko ? 1 : 0;
   return st;
 }
 
