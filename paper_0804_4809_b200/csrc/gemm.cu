@@ -117,6 +117,7 @@ cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
   a.C = op.C; a.ldc = op.ldc; a.c_bstride = op.c_bstride; a.split_stride = op.split_stride;
   a.C0 = op.C0; a.ldc0 = op.ldc0; a.c0_bstride = op.c0_bstride;
   a.alpha = op.alpha; a.M = op.M; a.N = op.N; a.K = op.K; a.K_dev = op.K_dev;
+  a.k_lo_mode = op.k_lo_mode; a.k_hi_mode = op.k_hi_mode; a.k_lo_dev = op.k_lo_dev;
   a.lower = op.lower; a.mirror = op.mirror; a.splits = op.splits < 1 ? 1 : op.splits;
   if (op.tile == TILE_128x32) {
     if (op.a_kmajor && op.b_kmajor) return launch<128, 32, 32, 32, 6, true, true>(op, a, st);

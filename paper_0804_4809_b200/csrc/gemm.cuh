@@ -31,6 +31,10 @@ struct GemmArgs {
   double alpha;
   int M, N, K;              // K ignored if K_dev
   const int *K_dev;         // device-resident K (panel update: the running rank r0)
+  int k_lo_mode, k_hi_mode;  // structured zeros of a triangular operand: the k-range of a tile is
+                             //   lo: 1 -> k >= m0, 2 -> k >= n0, 3 -> k >= k_lo_dev[m0];
+                             //   hi: 1 -> k < m0 + BM, 2 -> k < #{j : k_lo_dev[j] < m0 + BM}
+  const int *k_lo_dev;       // mode 3: first nonzero k of each operand column (L'L: pivot rows)
   int mtiles, ntiles;
   int mband;                // M-tiles per raster band (non-lower): a band of A stays L2-resident while N sweeps
   int lower;                // 1: enumerate lower-triangle tiles of a square output (M == N)
@@ -93,10 +97,27 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
   const int m0 = tm * BM, n0 = tn * BN;
   const int K = p.K_dev ? *p.K_dev : p.K;
   const int nslab_all = (K + BK - 1) / BK;
-  const int per = (nslab_all + p.splits - 1) / p.splits;
-  const int s_begin = min(nslab_all, split * per);
-  const int s_end = min(nslab_all, s_begin + per);
-  const int nslab = s_end - s_begin;
+  // k-range of this tile: [klo, khi) in slabs (triangular operands skip their zero blocks)
+  int klo = 0, khi = nslab_all;
+  if (p.k_lo_mode == 1) klo = m0 / BK;
+  else if (p.k_lo_mode == 2) klo = n0 / BK;
+  else if (p.k_lo_mode == 3) klo = (m0 < p.M ? p.k_lo_dev[m0] : K) / BK;
+  if (p.k_hi_mode == 1) khi = min(khi, (m0 + BM + BK - 1) / BK);
+  if (p.k_hi_mode == 2) {   // k < #{j : k_lo_dev[j] < m0 + BM}  (k_lo_dev increasing, length K)
+    int lo = 0, hi = K;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (p.k_lo_dev[mid] < m0 + BM) lo = mid + 1;
+      else hi = mid;
+    }
+    khi = min(khi, (lo + BK - 1) / BK);
+  }
+  klo = min(klo, khi);
+  const int nrange = khi - klo;
+  const int per = (nrange + p.splits - 1) / p.splits;
+  const int s_begin = klo + min(nrange, split * per);
+  const int s_end = min(khi, s_begin + per);
+  const int nslab = max(0, s_end - s_begin);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {

@@ -22,6 +22,8 @@ struct GemmOp {
   double alpha = 1.0;
   int M = 0, N = 0, K = 0;
   const int *K_dev = nullptr;   // device-side K (overrides K; K is then the upper bound)
+  int k_lo_mode = 0, k_hi_mode = 0;  // per-tile k-range of a triangular operand (see GemmArgs)
+  const int *k_lo_dev = nullptr;
   int batch = 1;
   bool lower = false, mirror = false;
   int splits = 1; long long split_stride = 0;

@@ -247,6 +247,7 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   op.K = r_pad;
   op.lower = true;
   op.mirror = true;
+  op.k_lo_mode = 1;                                    // C^-1 lower: Ci[k][i] = 0 for k < i
   op.C = M;
   op.ldc = ldm;
   GI_TRY(gemm(op, h->st));
@@ -272,6 +273,8 @@ geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true) {
   b.M = b.N = r;
   b.K = s;
   b.lower = true;
+  b.k_lo_mode = 3;                                     // L[k][i] = 0 above the pivot row piv[i] (Eq. 1)
+  b.k_lo_dev = h->piv;
   b.C = h->Bm;
   b.ldc = ld;
   GI_TRY(gemm(b, h->st));
@@ -287,6 +290,8 @@ geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true) {
   k.M = s;
   k.N = r;
   k.K = r;
+  k.k_hi_mode = 2;                                     // L[i][j] = 0 for rows i < piv[j] (Eq. 1)
+  k.k_lo_dev = h->piv;
   k.C = h->Kb;
   k.ldc = ld;
   GI_TRY(gemm(k, h->st));

@@ -79,6 +79,7 @@ cudaError_t trtri_lower(double *C, long long ldc, int r, double *Ci, long long l
       op1.N = h;
       op1.K = h;
       op1.batch = gr.count;
+      op1.k_lo_mode = 2;                               // Cinv11 lower: B(k, n) = 0 for k < n
       e = gemm(op1, st);
       if (e != cudaSuccess) return e;
       // Cinv21 = -Cinv22 * T1   (h2 x h)
@@ -95,6 +96,7 @@ cudaError_t trtri_lower(double *C, long long ldc, int r, double *Ci, long long l
       op2.N = h;
       op2.K = gr.h2;
       op2.batch = gr.count;
+      op2.k_hi_mode = 1;                               // Cinv22 lower: A(m, k) = 0 for k > m
       e = gemm(op2, st);
       if (e != cudaSuccess) return e;
     }
