@@ -157,13 +157,25 @@ geninv_status gram(geninv_handle h, const double *G, long long m, long long n, l
   const long long tiles = mt * (mt + 1) / 2;
   int S = pick_splits(tiles, (ell + 15) / 16);
   // accuracy: no partial sum runs over more than 2^17 rows of G (each DMMA tile accumulates its
-  // k-range sequentially); the fixed-order reduction then adds <= 16 partials.  Capped so the
-  // partial slices stay within ~2.5 GB.
+  // k-range sequentially); the fixed-order reduction then adds the partials.  When that asks for
+  // splits anyway, the count is rounded to the one (up to 48, partial slices within ~6 GB) with
+  // the best last-wave fill of the tiles x splits CTAs (C4: 37 -> exactly 132 waves of 148).
   {
     const long long pbytes = (long long)h->ld * h->ld * 8;
     const int s_acc = (int)std::min<long long>(16, (ell + (1LL << 17) - 1) >> 17);
-    const int s_cap = (int)std::max<long long>(1, (2560LL << 20) / pbytes);
+    const int s_cap = (int)std::max<long long>(1, (6144LL << 20) / pbytes);
     S = std::min(std::max(S, s_acc), std::max(S, s_cap));
+    if (s_acc > 1 && ell / (16LL * 48) >= 16) {
+      const int sms = num_sms();
+      double best = -1.0;
+      int bs = S;
+      for (int c = S; c <= std::min(48, s_cap); ++c) {
+        const long long work = tiles * c, waves = (work + sms - 1) / sms;
+        const double eff = (double)work / (double)(waves * sms);
+        if (eff > best + 1e-9) { best = eff; bs = c; }
+      }
+      S = bs;
+    }
   }
   if (S == 1 && !accumulate) {
     op.C = A;
