@@ -23,6 +23,14 @@ using namespace gi;
 struct geninv_handle_s {
   int device = 0;
   cudaStream_t own = nullptr, st = nullptr, st2 = nullptr, upd = nullptr;
+  // CUDA graphs of the launch-bound factorisation chain (replayed while the shapes/pointers match)
+  struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    long long key[10] = {};
+    long long nlaunch = 0;   // kernels in the graph (counted while capturing)
+  } g_factor, g_build;
+  cudaStream_t gstream = nullptr;   // private non-blocking stream the graphs are captured / launched on
+  cudaEvent_t ev_g[2] = {};
   cudaEvent_t ev[4] = {};
   cudaEvent_t ev_fr[4] = {};  // frchol lookahead events
   // s x s workspaces (leading dimension ld >= round_up(s, 32))
@@ -225,11 +233,68 @@ double tol_rel_of(const geninv_opts *o) { return o ? o->tol_rel : 1e-9; }
 double tol_abs_of(const geninv_opts *o) { return o ? o->tol_abs : -1.0; }
 
 // a2 + a3 on h->A-like input; L zeroed here.  Returns rank via host sync.
+bool graphs_on() {
+  static const bool on = [] {
+    const char *e = getenv("GENINV_NO_GRAPH");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
+}
+
+// Run `enqueue(stream)` as a CUDA graph on the handle's private stream, ordered after / before the
+// work of h->st by events: captured on first use, replayed while `key` matches (same shapes and
+// buffers).  The panel chain is ~4 launches per 32 columns; as a graph the host submits it once.
+template <typename F>
+geninv_status run_graph(geninv_handle h, geninv_handle_s::GraphSlot &slot, const long long (&key)[10], F enqueue) {
+  if (!graphs_on()) return enqueue(h->st);
+  cudaStream_t gs = h->gstream;
+  GI_TRY(cudaEventRecord(h->ev_g[0], h->st));
+  GI_TRY(cudaStreamWaitEvent(gs, h->ev_g[0], 0));
+  bool hit = slot.exec != nullptr;
+  for (int i = 0; i < 10 && hit; ++i) hit = slot.key[i] == key[i];
+  if (!hit) {
+    if (slot.exec) cudaGraphExecDestroy(slot.exec);
+    slot.exec = nullptr;
+    cudaGraph_t g = nullptr;
+    GI_TRY(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+    const long long l0 = h->launches;
+    geninv_status st = enqueue(gs);
+    slot.nlaunch = h->launches - l0;
+    h->launches = l0;
+    cudaError_t e = cudaStreamEndCapture(gs, &g);
+    if (st != GENINV_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    GI_TRY(e);
+    e = cudaGraphInstantiate(&slot.exec, g, 0);
+    cudaGraphDestroy(g);
+    GI_TRY(e);
+    for (int i = 0; i < 10; ++i) slot.key[i] = key[i];
+  }
+  GI_TRY(cudaGraphLaunch(slot.exec, gs));
+  h->launches += slot.nlaunch;
+  GI_TRY(cudaEventRecord(h->ev_g[1], gs));
+  GI_TRY(cudaStreamWaitEvent(h->st, h->ev_g[1], 0));
+  return GENINV_OK;
+}
+
+long long dbits(double x) {
+  long long v;
+  memcpy(&v, &x, sizeof(v));
+  return v;
+}
+
 geninv_status factor(geninv_handle h, const double *A, long long lda, int s, double *L, long long ldl, int *piv,
                      const geninv_opts *opts, int *rank_out, FactorStats *hst) {
-  GI_TRY(tolerance(A, lda, s, tol_rel_of(opts), tol_abs_of(opts), h->fs, h->st));
-  GI_TRY(cudaMemsetAsync(L, 0, (size_t)s * ldl * sizeof(double), h->st));
-  GI_TRY(frchol(A, lda, s, L, ldl, piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, h->st, h->upd, h->ev_fr));
+  const long long key[10] = {(long long)(uintptr_t)A, lda, s, (long long)(uintptr_t)L, ldl, (long long)(uintptr_t)piv,
+                             dbits(tol_rel_of(opts)), dbits(tol_abs_of(opts)), h->ld, 1};
+  GI_TRYS(run_graph(h, h->g_factor, key, [&](cudaStream_t st) -> geninv_status {
+    GI_TRY(tolerance(A, lda, s, tol_rel_of(opts), tol_abs_of(opts), h->fs, st));
+    GI_TRY(cudaMemsetAsync(L, 0, (size_t)s * ldl * sizeof(double), st));
+    GI_TRY(frchol(A, lda, s, L, ldl, piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, st, h->upd, h->ev_fr));
+    return GENINV_OK;
+  }));
   const int np = (s + PB - 1) / PB;
   h->launches += 1 + np + 2 * std::max(0, np - 2);
   int r = 0;
@@ -436,7 +501,15 @@ geninv_status from_gram(geninv_handle h, const double *A, int s, long long lda, 
   if (st != GENINV_OK) return st;
   const bool ko = ell > 0 && k_order && k_order_cheaper(s, ell, r);
   if (k_order) *k_order = ko;
-  GI_TRYS(build_x(h, s, r, !ko));
+  // a4-a6 (L'L, the SPD inverse's panel chain, TRTRI, the products) as one CUDA graph per (s, r)
+  const long long key[10] = {s, r, ko ? 0 : 1, h->ld, (long long)(uintptr_t)h->L, 2, 0, 0, 0, 0};
+  GI_TRYS(run_graph(h, h->g_build, key, [&](cudaStream_t st) -> geninv_status {
+    cudaStream_t saved = h->st;
+    h->st = st;
+    const geninv_status rs = build_x(h, s, r, !ko);
+    h->st = saved;
+    return rs;
+  }));
   h->x_s = ko ? -1 : s;
   h->last_rank = r;
   *r_out = r;
@@ -485,6 +558,8 @@ geninv_status geninv_create(geninv_handle *out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->upd, cudaStreamNonBlocking);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_fr[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_g[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete h;
     return cuda_status(e);
@@ -515,6 +590,11 @@ geninv_status geninv_destroy(geninv_handle h) {
   for (auto &ev : h->ev_fr)
     if (ev) cudaEventDestroy(ev);
   if (h->upd) cudaStreamDestroy(h->upd);
+  if (h->g_factor.exec) cudaGraphExecDestroy(h->g_factor.exec);
+  if (h->g_build.exec) cudaGraphExecDestroy(h->g_build.exec);
+  for (auto &ev : h->ev_g)
+    if (ev) cudaEventDestroy(ev);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
   if (h->st2) cudaStreamDestroy(h->st2);
   if (h->own) cudaStreamDestroy(h->own);
   delete h;

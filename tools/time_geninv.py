@@ -30,4 +30,4 @@ for _ in range(reps):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 print(f"{name} geninv_d: median {np.median(ts):.3f} ms  min {np.min(ts):.3f} ms  rank {info.rank}  "
-      f"overlap {'off' if os.environ.get('GENINV_NO_OVERLAP') else 'on'}")
+      f"graphs {'off' if os.environ.get('GENINV_NO_GRAPH') else 'on'}")
