@@ -531,13 +531,13 @@ bool is_small(long long m, long long n) { return std::min(m, n) <= 64 && std::ma
 geninv_status small_path(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
                          long long ldp, const geninv_opts *opts, int *r_out, FactorStats *fs) {
   GI_TRYS(ensure_ws(h, 64));
-  GI_TRY(batched_geninv(G, (int)m, (int)n, ld, 0, 1, Gp, ldp, 0, h->rk, tol_rel_of(opts), tol_abs_of(opts), h->st,
-                        h->fs));
+  // the rank goes to the stats record's spare int, so one copy returns both
+  GI_TRY(batched_geninv(G, (int)m, (int)n, ld, 0, 1, Gp, ldp, 0, &h->fs->pad, tol_rel_of(opts), tol_abs_of(opts),
+                        h->st, h->fs));
   h->launches += 1;
-  int rr = 0;
-  GI_TRY(cudaMemcpyAsync(&rr, h->rk, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   GI_TRY(cudaMemcpyAsync(fs, h->fs, sizeof(FactorStats), cudaMemcpyDeviceToHost, h->st));
   GI_TRY(cudaStreamSynchronize(h->st));
+  const int rr = fs->pad;
   h->x_s = -1;
   *r_out = rr < 0 ? 0 : rr;
   return rr == -2 ? GENINV_ENONFINITE : rr == -3 ? GENINV_ENOTSPD : GENINV_OK;

@@ -13,7 +13,7 @@ struct FactorStats {
   double min_pivot;  // min pivot
   double tol;        // tolerance used
   int flags;         // bit0: non-finite diagonal, bit1: non-SPD pivot (mode 1)
-  int pad;
+  int pad;           // spare (the one-CTA small path stores the rank here)
 };
 
 // a2: tol = tol_abs >= 0 ? tol_abs : tol_rel * min{A_ii > 0} (0 if none); also
