@@ -66,10 +66,13 @@ geninv_status cuda_status(cudaError_t e) {
   return GENINV_ECUDA;
 }
 
-#define GI_TRY(expr)                                  \
-  do {                                                \
-    cudaError_t _e = (expr);                          \
-    if (_e != cudaSuccess) return cuda_status(_e);    \
+#define GI_TRY(expr)                                                             \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      fprintf(stderr, "[geninv] %s:%d: %s\n", __FILE__, __LINE__, #expr);        \
+      return cuda_status(_e);                                                    \
+    }                                                                            \
   } while (0)
 
 #define GI_TRYS(expr)                                 \
@@ -694,20 +697,31 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
     h->gdev_bytes = gbytes;
   }
   GI_TRYS(ensure_ws(h, s));
-  // ---- H2D in row chunks, the Gram of each chunk accumulated as soon as it lands
-  //      (N branch: A = sum_c G_c' G_c; T branch: the Gram needs all columns -> one pass after the copy)
-  const long long rows_per = tr ? m : std::max<long long>(1, (256LL << 20) / (ldg * 8));
-  int nch = 0;
-  for (long long r0 = 0; r0 < m; r0 += rows_per, ++nch) {
-    const long long rows = std::min(rows_per, m - r0);
-    GI_TRY(cudaMemcpy2DAsync(h->Gdev + r0 * ldg, ldg * 8, G_host + r0 * ld, ld * 8, n * 8, rows,
-                             cudaMemcpyHostToDevice, h->st2));
-    GI_TRY(cudaEventRecord(h->ev[0], h->st2));
-    GI_TRY(cudaStreamWaitEvent(h->st, h->ev[0], 0));
-    if (!tr)
+  // ---- H2D in chunks of ~1/16 of G (32 .. 256 MB), the Gram of each chunk accumulated as soon as it
+  //      lands: N branch row chunks (A = sum_c G_c' G_c), T branch column chunks (A = sum_c G_c G_c'),
+  //      summed in chunk order (deterministic)
+  const long long target = std::min<long long>(256LL << 20, std::max<long long>(32LL << 20, (long long)gbytes / 16));
+  if (!tr) {
+    const long long rows_per = std::max<long long>(1, target / (ldg * 8));
+    for (long long r0 = 0; r0 < m; r0 += rows_per) {
+      const long long rows = std::min(rows_per, m - r0);
+      GI_TRY(cudaMemcpy2DAsync(h->Gdev + r0 * ldg, ldg * 8, G_host + r0 * ld, ld * 8, n * 8, rows,
+                               cudaMemcpyHostToDevice, h->st2));
+      GI_TRY(cudaEventRecord(h->ev[0], h->st2));
+      GI_TRY(cudaStreamWaitEvent(h->st, h->ev[0], 0));
       GI_TRYS(gram(h, h->Gdev + r0 * ldg, rows, n, ldg, 0, h->A, h->ld, r0 == 0 ? nullptr : h->A));
+    }
+  } else {
+    const long long cols_per = std::max<long long>(16, target / (m * 8) / 16 * 16);
+    for (long long c0 = 0; c0 < n; c0 += cols_per) {
+      const long long cols = std::min(cols_per, n - c0);
+      GI_TRY(cudaMemcpy2DAsync(h->Gdev + c0, ldg * 8, G_host + c0, ld * 8, cols * 8, m, cudaMemcpyHostToDevice,
+                               h->st2));
+      GI_TRY(cudaEventRecord(h->ev[0], h->st2));
+      GI_TRY(cudaStreamWaitEvent(h->st, h->ev[0], 0));
+      GI_TRYS(gram(h, h->Gdev + c0, m, cols, ldg, 1, h->A, h->ld, c0 == 0 ? nullptr : h->A));
+    }
   }
-  if (tr) GI_TRYS(gram(h, h->Gdev, m, n, ldg, 1, h->A, h->ld));
   int r = 0;
   FactorStats fs{};
   geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs);
@@ -718,9 +732,10 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
   }
   // ---- output in chunks, D2H of chunk c overlapped with the product of chunk c + 1
   //      N: column block j0..j1 of G+ (n x m) = X G[j0:j1]';  T: row block of G+ = G[:, i0:i1]' X
-  const long long cw = tr ? std::max<long long>(1, (256LL << 20) / (m * 8)) : rows_per;
+  // chunk width: a multiple of 16 (even leading dimension of the G+ chunk; 16-aligned TMA strips)
+  const long long cw = std::max<long long>(16, (tr ? target / (m * 8) : target / (ldg * 8)) / 16 * 16);
   const long long total = tr ? n : m;
-  const size_t cbytes = (size_t)cw * s * sizeof(double) + 256;
+  const size_t cbytes = (size_t)cw * (s + 1) * sizeof(double) + 256;
   if (cbytes > h->chunk_bytes) {
     for (auto &c : h->Gpchunk) {
       if (c) cudaFree(c);

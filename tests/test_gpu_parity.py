@@ -282,3 +282,19 @@ def test_batched_deterministic(H):
         torch.cuda.synchronize()
         assert torch.equal(rk, rref)
         assert torch.equal(Gp, ref)
+
+
+@pytest.mark.parametrize("m,n,r", [(40000, 300, 250), (300, 40000, 250)])
+def test_host_buffers_chunked(H, m, n, r):
+    # ~96 MB inputs: the host path copies and accumulates the Gram in 3 chunks (rows for m >= n,
+    # columns for m < n) and streams G+ back in chunks; same result as the device path
+    G = I.low_rank(m + 2 * n, m, n, r).numpy()
+    dev_gp, dev_info = run(H, G)
+    Gh = torch.as_tensor(G).pin_memory()
+    Gph = torch.empty(n, m, dtype=torch.float64).pin_memory()
+    _, info = H.geninv_host_d(Gh, Gph)
+    assert info.rank == dev_info.rank == r
+    assert C.rel_fro(Gph.numpy(), dev_gp) <= 1e-10
+    R = O.geninv(G)
+    if R.in_Q():
+        assert C.rel_fro(Gph.numpy(), R.Gp) <= REL
