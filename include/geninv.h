@@ -94,7 +94,7 @@ GENINV_API const char *geninv_strerror(geninv_status st);
  * rank (host, may be NULL) receives r; info (host, may be NULL) diagnostics.
  * Zero G -> rank 0 and G+ = 0 (reading R2).  Synchronises the stream.
  * Small matrices (min(m, n) <= 64, max(m, n) <= 128) run the whole path in one
- * CTA (the batched kernel, a9); that path does not keep X in the handle
+ * CTA (the batched kernel, a9; any alignment and leading dimension); that path does not keep X in the handle
  * (geninv_copy_x then returns GENINV_ESTATE).  For low rank, where
  * 4 r s l < s (s + 1) r + 2 s^2 l (s = min(m, n), l = max(m, n)), geninv_d skips
  * X and evaluates G+ = K (K' G') (m >= n) or (G' K) K' (m < n) with K = L M,

@@ -621,7 +621,11 @@ const char *geninv_strerror(geninv_status st) {
 geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp, int64_t ldp,
                        int64_t *rank, const geninv_opts *opts, geninv_info *info) {
   if (!h || !Gp || ldp < m) return GENINV_EINVAL;
-  GI_TRYS(check_g(G, m, n, ld));
+  {
+    const geninv_status cs = check_g(G, m, n, ld);
+    // the one-CTA small path stages G with 8-byte copies when needed: any alignment / ld is fine there
+    if (cs != GENINV_OK && !(cs == GENINV_EALIGN && is_small(m, n))) return cs;
+  }
   cudaSetDevice(h->device);
   const int tr = m < n;  // P:109 (strict; m == n takes the N branch, R6)
   const int s = (int)(tr ? m : n);

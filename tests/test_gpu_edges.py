@@ -1,0 +1,110 @@
+"""Degenerate and boundary inputs through the C ABI (`-m gpu`): vectors, rank 0 and 1, the
+small / general path boundary, padded and odd leading dimensions, strided batches, invalid
+arguments.  Expected values come from the oracle (or exact closed forms)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import checks as C
+from oracle import geninv_oracle as O
+from paper_0804_4809_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_0804_4809_b200.binding import Handle
+    return Handle(0)
+
+
+def dev(X, pad=0):
+    m, n = X.shape
+    t = torch.zeros(m, n + pad, dtype=torch.float64, device="cuda")
+    t[:, :n] = torch.as_tensor(X)
+    return t[:, :n]
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (1, 7), (9, 1), (1, 300), (500, 1), (2, 2)])
+def test_vectors_and_tiny(H, m, n):
+    G = I.dense_normal(m * 100 + n, m, n).numpy()
+    Gp, info = H.geninv_d(dev(G, pad=(n & 1)))
+    R = O.geninv(G)
+    assert info.rank == R.rank == min(m, n)
+    assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-12
+
+
+def test_rank_one_closed_form(H):
+    # G = u v': G+ = v u' / (|u|^2 |v|^2)
+    u = I.dense_normal(1, 200, 1).numpy()
+    v = I.dense_normal(2, 90, 1).numpy()
+    G = u @ v.T
+    Gp, info = H.geninv_d(dev(G))
+    assert info.rank == 1
+    want = (v @ u.T) / (float((u.T @ u)[0, 0]) * float((v.T @ v)[0, 0]))
+    assert C.rel_fro(Gp.cpu().numpy(), want) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n", [(64, 64), (128, 64), (64, 128), (129, 64), (64, 65), (65, 64)])
+def test_small_path_boundary(H, m, n):
+    # min(m, n) <= 64 and max(m, n) <= 128 run the one-CTA kernel, the rest the general path
+    r = min(m, n) - 3
+    G = I.low_rank(m * 7 + n, m, n, r).numpy()
+    R = O.geninv(G)
+    small = min(m, n) <= 64 and max(m, n) <= 128
+    Gp, info = H.geninv_d(dev(G, pad=1 if small else (n & 1)))   # odd ld only where the small path runs
+    assert info.rank == R.rank
+    if R.in_Q():
+        assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
+
+
+def test_zero_matrix_both_paths(H):
+    for (m, n) in ((50, 30), (600, 300), (300, 600)):
+        Gp = torch.full((n, m), 3.0, dtype=torch.float64, device="cuda")
+        _, info = H.geninv_d(torch.zeros(m, n, dtype=torch.float64, device="cuda"), Gp)
+        assert info.rank == 0 and bool((Gp == 0).all())
+
+
+def test_batched_strided_and_odd_ld(H):
+    # a batch stored with padding between matrices and an odd leading dimension (8-byte copies)
+    cfg = I.CONFIGS["C1"]
+    base = torch.zeros(5, 64 + 3, 49, dtype=torch.float64, device="cuda")
+    for i in range(5):
+        base[i, :64, :48] = I.make_single(cfg, i + 1).cuda()
+    G = base[:, :64, :48]                          # ld 49 (odd), stride 67 * 49
+    Gp, rk = H.geninv_batched_d(G)
+    torch.cuda.synchronize()
+    for i in range(5):
+        R = O.geninv(G[i].cpu().numpy())
+        assert int(rk[i]) == R.rank
+        assert C.rel_fro(Gp[i].cpu().numpy(), R.Gp) <= 1e-9
+
+
+def test_batched_rank_zero_and_mixed(H):
+    cfg = I.CONFIGS["C1"]
+    Gs = torch.stack([I.make_single(cfg, 1), torch.zeros(64, 48, dtype=torch.float64),
+                      I.low_rank(3, 64, 48, 1)]).cuda()
+    Gp, rk = H.geninv_batched_d(Gs)
+    torch.cuda.synchronize()
+    assert rk.tolist() == [32, 0, 1]
+    assert bool((Gp[1] == 0).all())
+    for i in (0, 2):
+        assert C.rel_fro(Gp[i].cpu().numpy(), O.geninv(Gs[i].cpu().numpy()).Gp) <= 1e-9
+
+
+def test_invalid_arguments(H):
+    from paper_0804_4809_b200.binding import GeninvError
+    lib = H._lib
+    G = torch.zeros(10, 4, dtype=torch.float64, device="cuda")
+    Gp = torch.zeros(4, 10, dtype=torch.float64, device="cuda")
+    # ld < n, ldp < m, m = 0, too large batched shapes -> GENINV_EINVAL (1)
+    assert lib.geninv_d(H._h, G.data_ptr(), 10, 4, 3, Gp.data_ptr(), 10, None, None, None) == 1
+    assert lib.geninv_d(H._h, G.data_ptr(), 10, 4, 4, Gp.data_ptr(), 9, None, None, None) == 1
+    assert lib.geninv_d(H._h, G.data_ptr(), 0, 4, 4, Gp.data_ptr(), 10, None, None, None) == 1
+    big = torch.zeros(2, 65, 65, dtype=torch.float64, device="cuda")
+    with pytest.raises(GeninvError):
+        H.geninv_batched_d(big)
+    # split API: apply before any factorisation of that size -> GENINV_ESTATE (7)
+    from paper_0804_4809_b200.binding import Handle
+    h2 = Handle(0)
+    assert h2._lib.geninv_apply_d(h2._h, G.data_ptr(), 10, 4, 4, 0, Gp.data_ptr(), 10) == 7
