@@ -56,7 +56,8 @@ typedef enum {
   GENINV_ECUDA = 4,       /* CUDA runtime / launch error */
   GENINV_ENOMEM = 5,      /* device allocation failed */
   GENINV_EALIGN = 6,      /* pointer not 16-byte aligned or odd leading dimension */
-  GENINV_ESTATE = 7       /* geninv_apply_d before geninv_from_gram_d, or shape mismatch */
+  GENINV_ESTATE = 7,      /* geninv_apply_d before geninv_from_gram_d, or shape mismatch */
+  GENINV_ENCCL = 8        /* geninv_sharded_d: libnccl.so.2 not loadable or ncclAllReduce failed */
 } geninv_status;
 
 /* Tolerance policy (SPEC ToleranceConfig).  NULL opts = the paper's policy. */
@@ -132,6 +133,22 @@ GENINV_API geninv_status geninv_batched_d(geninv_handle h, const double *G, int6
 GENINV_API geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld,
                              const double *F, int64_t k, int64_t ldf, double *W, int64_t ldw, int64_t *rank,
                              const geninv_opts *opts, geninv_info *info);
+
+/* ---- sharded multi-GPU step (a8, north star: "G is row-sharded") ----------
+ * One process per GPU.  trans == 0 (tall G, C4): G_local = this rank's rows
+ * (m_local x n, ld), Gp_local = this rank's column block of G+ (n x m_local,
+ * ldp >= m_local).  trans == 1 (wide G, C3): G_local = this rank's
+ * columns (m x n_local passed as m_local = m, n = n_local), Gp_local = its row
+ * block of G+ (n_local x m, ldp >= m).  The local Gram A_p is summed over the
+ * ranks with one ncclAllReduce (FP64, sum) on the handle's stream; the
+ * factorisation and inverse run replicated (deterministic: every rank gets the
+ * same r and X); the output needs no further communication.  nccl_comm is an
+ * ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()); NCCL is resolved at
+ * run time from the already-loaded libnccl.so.2 (GENINV_ENCCL if absent).
+ * Synchronises; rank / info as for geninv_d. */
+GENINV_API geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G_local, int64_t m_local,
+                               int64_t n, int64_t ld, int32_t trans, double *Gp_local, int64_t ldp, int64_t *rank,
+                               const geninv_opts *opts, geninv_info *info);
 
 /* ---- split form (row sharding, a8) -----------------------------------------
  * geninv_gram_d: A (s x s, lda >= s, device, caller-owned) = G'G if trans == 0

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GENINV_LIB", os.path.join(_HERE, "libgeninv.so"))  # instrumented builds only
 
 GENINV_OK, GENINV_EINVAL, GENINV_ENONFINITE, GENINV_ENOTSPD, GENINV_ECUDA, GENINV_ENOMEM, GENINV_EALIGN, \
-    GENINV_ESTATE = range(8)
+    GENINV_ESTATE, GENINV_ENCCL = range(9)
 
 
 class GeninvError(RuntimeError):
@@ -82,6 +82,9 @@ _SIGS = {
     "geninv_spd_inverse_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                              ctypes.c_int64],
     "geninv_copy_x": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
+    "geninv_sharded_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                         ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                         ctypes.c_void_p, ctypes.c_void_p],
     "geninv_solve_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
@@ -213,6 +216,18 @@ class Handle:
                                         _dev(W, "W"), W.stride(0), ctypes.byref(rank), ctypes.byref(o),
                                         ctypes.byref(info)))
         return W, _info(info)
+
+    def geninv_sharded_d(self, nccl_comm: int, G_local: torch.Tensor, trans: int, Gp_local: torch.Tensor,
+                         tol_rel=1e-9, tol_abs=-1.0):
+        """One sharded step (local Gram, ncclAllReduce of A, replicated factorisation, local block of G+)."""
+        m, n = G_local.shape
+        info = _Info()
+        rank = ctypes.c_int64()
+        o = _opts(tol_rel, tol_abs)
+        _check(self._lib.geninv_sharded_d(self._h, ctypes.c_void_p(nccl_comm), _dev(G_local, "G"), m, n,
+                                          G_local.stride(0), int(trans), _dev(Gp_local, "Gp"), Gp_local.stride(0),
+                                          ctypes.byref(rank), ctypes.byref(o), ctypes.byref(info)))
+        return Gp_local, _info(info)
 
     # ---------------------------------------------------------------- split form
     def geninv_gram_d(self, G: torch.Tensor, trans: int, A: torch.Tensor):

@@ -12,6 +12,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 
 #include "../../include/geninv.h"
@@ -614,6 +616,7 @@ const char *geninv_strerror(geninv_status st) {
     case GENINV_ENOMEM: return "device out of memory";
     case GENINV_EALIGN: return "pointer not 16-byte aligned or odd leading dimension";
     case GENINV_ESTATE: return "no factorisation of matching size in the handle";
+    case GENINV_ENCCL: return "NCCL unavailable or the all-reduce failed";
   }
   return "unknown status";
 }
@@ -804,6 +807,48 @@ geninv_status geninv_batched_d(geninv_handle h, const double *G, int64_t m, int6
                         tol_abs_of(opts), h->st));
   h->launches += 1;
   return GENINV_OK;
+}
+
+// ---- NCCL, resolved at run time (the library itself does not link NCCL): the communicator comes
+//      from the caller (e.g. torch's ProcessGroupNCCL), so the already-loaded libnccl is reused.
+typedef int (*nccl_allreduce_fn)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+static nccl_allreduce_fn nccl_allreduce() {
+  static nccl_allreduce_fn fn = [] {
+    void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    return lib ? reinterpret_cast<nccl_allreduce_fn>(dlsym(lib, "ncclAllReduce")) : nullptr;
+  }();
+  return fn;
+}
+
+geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G_local, int64_t m_local, int64_t n,
+                               int64_t ld, int32_t trans, double *Gp_local, int64_t ldp, int64_t *rank,
+                               const geninv_opts *opts, geninv_info *info) {
+  if (!h || !nccl_comm || !Gp_local) return GENINV_EINVAL;
+  GI_TRYS(check_g(G_local, m_local, n, ld));
+  const long long s = trans ? m_local : n;
+  if (ldp < (trans ? s : m_local)) return GENINV_EINVAL;
+  nccl_allreduce_fn ar = nccl_allreduce();
+  if (!ar) return GENINV_ENCCL;
+  cudaSetDevice(h->device);
+  GI_TRYS(ensure_ws(h, (int)s));
+  // a1 on the local block, into a zeroed A (the all-reduced upper triangle stays exactly zero)
+  GI_TRY(cudaMemsetAsync(h->A, 0, (size_t)s * h->ld * sizeof(double), h->st));
+  GI_TRYS(gram(h, G_local, m_local, n, ld, trans, h->A, h->ld));
+  // a8: A = sum_p A_p -- the one exchange step (NCCL over NVLink / NVSwitch), FP64 sum
+  if (ar(h->A, h->A, (size_t)s * h->ld, /*ncclFloat64*/ 8, /*ncclSum*/ 0, nccl_comm, h->st) != 0) return GENINV_ENCCL;
+  int r = 0;
+  FactorStats fs{};
+  geninv_status st = from_gram(h, h->A, (int)s, h->ld, opts, &r, &fs);   // a2-a6, replicated
+  if (st == GENINV_OK) st = finish_spd_check(h, r);
+  if (st == GENINV_OK) st = apply(h, G_local, m_local, n, ld, trans, Gp_local, ldp, h->st);   // a7, local block
+  if (st == GENINV_OK) {
+    cudaError_t e = cudaStreamSynchronize(h->st);
+    if (e != cudaSuccess) st = cuda_status(e);
+  }
+  if (rank) *rank = r;
+  fill_info(info, fs, r, trans, st);
+  return st;
 }
 
 geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, const double *F,

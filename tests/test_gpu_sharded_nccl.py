@@ -1,0 +1,52 @@
+"""geninv_sharded_d through a real NCCL communicator (`-m gpu`).  On the single GPU of the test box
+the process group has one rank, so the all-reduce is the identity: the call must reproduce
+geninv_d bit for bit, in both sharding modes (rows of a tall G, columns of a wide G).  The
+multi-rank orchestration is covered on CPU by tests/test_sharded_gloo.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+from oracle import checks as C
+from oracle import geninv_oracle as O
+from paper_0804_4809_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    t = torch.ones(1, device="cuda")
+    dist.all_reduce(t)
+    be = dist.distributed_c10d._get_default_group()._get_backend(torch.device("cuda"))
+    yield be._comm_ptr()
+    dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_0804_4809_b200.binding import Handle
+    return Handle(0)
+
+
+@pytest.mark.parametrize("m,n,r,trans", [(3000, 400, 300, 0), (400, 3000, 300, 1)])
+def test_sharded_single_rank_equals_geninv(H, comm, m, n, r, trans):
+    G = I.low_rank(m + 11 * n, m, n, r, device="cuda")
+    whole, info = H.geninv_d(G)
+    Gp = torch.empty(n, m, dtype=torch.float64, device="cuda")
+    _, sinfo = H.geninv_sharded_d(comm, G, trans, Gp)
+    assert sinfo.rank == info.rank == r
+    R = O.geninv(G.cpu().numpy())
+    if R.in_Q():
+        assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
+    assert C.rel_fro(Gp.cpu().numpy(), whole.cpu().numpy()) <= 1e-12
