@@ -103,6 +103,14 @@ GENINV_API const char *geninv_strerror(geninv_status st);
 GENINV_API geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp,
                        int64_t ldp, int64_t *rank, const geninv_opts *opts, geninv_info *info);
 
+/* Asynchronous variant: nothing is copied back and the stream is not synchronised.  rank_dev
+ * (device int64) receives r, or -GENINV_ENONFINITE / -GENINV_ENOTSPD; G+ is then unspecified.
+ * Without the rank on the host, the inverse runs at the full size s with an identity block past
+ * the detected rank (M = diag(M_r, I); K = L M and X = K K' are exactly the rank-r results), so
+ * it costs up to (s/r)^3 more inverse flops than geninv_d.  Always the X G' / G' X order. */
+GENINV_API geninv_status geninv_d_async(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp,
+                             int64_t ldp, int64_t *rank_dev, const geninv_opts *opts);
+
 /* Same computation with HOST buffers G_host (m x n, ld) and Gp_host (n x m, ldp):
  * the library stages G to the device in row chunks (copies overlapped with the
  * Gram), and streams G+ back overlapped with the output product.  Device

@@ -82,6 +82,8 @@ _SIGS = {
     "geninv_spd_inverse_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                              ctypes.c_int64],
     "geninv_copy_x": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p],
+    "geninv_d_async": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                       ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p],
     "geninv_sharded_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                          ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                          ctypes.c_void_p, ctypes.c_void_p],
@@ -172,6 +174,19 @@ class Handle:
         _check(self._lib.geninv_d(self._h, _dev(G, "G"), m, n, G.stride(0), _dev(Gp, "Gp"), Gp.stride(0),
                                   ctypes.byref(rank), ctypes.byref(o), ctypes.byref(info)))
         return Gp, _info(info)
+
+    def geninv_d_async(self, G: torch.Tensor, Gp: torch.Tensor | None = None, rank: torch.Tensor | None = None,
+                       tol_rel=1e-9, tol_abs=-1.0):
+        """G+ without host synchronisation -> (Gp, rank int64[1] on the device)."""
+        m, n = G.shape
+        if Gp is None:
+            Gp = torch.empty(n, m, dtype=torch.float64, device=G.device)
+        if rank is None:
+            rank = torch.empty(1, dtype=torch.int64, device=G.device)
+        o = _opts(tol_rel, tol_abs)
+        _check(self._lib.geninv_d_async(self._h, _dev(G, "G"), m, n, G.stride(0), _dev(Gp, "Gp"), Gp.stride(0),
+                                        ctypes.c_void_p(rank.data_ptr()), ctypes.byref(o)))
+        return Gp, rank
 
     def geninv_host_d(self, G: torch.Tensor, Gp: torch.Tensor, tol_rel=1e-9, tol_abs=-1.0):
         """Host-buffer variant (G, Gp CPU float64 tensors, ideally pinned)."""

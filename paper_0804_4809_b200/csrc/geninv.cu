@@ -30,7 +30,7 @@ struct geninv_handle_s {
     cudaGraphExec_t exec = nullptr;
     long long key[10] = {};
     long long nlaunch = 0;   // kernels in the graph (counted while capturing)
-  } g_factor, g_build;
+  } g_factor, g_build, g_async;
   cudaStream_t gstream = nullptr;   // private non-blocking stream the graphs are captured / launched on
   cudaEvent_t ev_g[2] = {};
   cudaEvent_t ev[4] = {};
@@ -340,8 +340,26 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   return GENINV_OK;
 }
 
+// ---- device-side rank (geninv_d_async): the chain runs at the full size s; past the detected rank
+//      the pivot list is padded with s (empty k-ranges) and B = L'L gets an identity block, so
+//      M = inv(diag(B_r, I)) = diag(M_r, I) and K = L M, X = K K' are exactly the rank-r results.
+__global__ void async_pad_kernel(int *piv, const int *rk_final, int s) {
+  const int r = *rk_final;
+  for (int i = r + blockIdx.x * blockDim.x + threadIdx.x; i < s; i += gridDim.x * blockDim.x) piv[i] = s;
+}
+__global__ void identity_tail_kernel(double *B, long long ldb, const int *rk_final, int s) {
+  const int r = *rk_final;
+  for (int i = r + blockIdx.x * blockDim.x + threadIdx.x; i < s; i += gridDim.x * blockDim.x)
+    B[(long long)i * ldb + i] = 1.0;
+}
+__global__ void async_rank_kernel(int64_t *out, const int *rk_final, const FactorStats *fs, const FactorStats *fs2) {
+  const int r = *rk_final;
+  *out = (fs->flags & 1) ? -(int64_t)GENINV_ENONFINITE : (r > 0 && (fs2->flags & 2)) ? -(int64_t)GENINV_ENOTSPD : r;
+}
+
 // a4-a6 after the factorisation: K = L M (s x r) and, if want_x, X (s x s, full) = K K' = L M M L'.
-geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true) {
+// rk_pad (device, optional): r is the full size s and the detected rank is *rk_pad (see above).
+geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true, const int *rk_pad = nullptr) {
   const long long ld = h->ld;
   if (r == 0) {
     GI_TRY(cudaMemsetAsync(h->X, 0, (size_t)s * ld * sizeof(double), h->st));
@@ -361,6 +379,11 @@ geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true) {
   b.ldc = ld;
   GI_TRY(gemm(b, h->st));
   h->launches += 1;
+  if (rk_pad) {
+    identity_tail_kernel<<<(s + 255) / 256, 256, 0, h->st>>>(h->Bm, ld, rk_pad, s);
+    GI_TRY(cudaGetLastError());
+    h->launches += 1;
+  }
   // a5
   GI_TRYS(spd_inverse(h, h->Bm, r, ld, h->Mm, ld));
   // a6: K = L M (s x r):  K[i][c] = sum_j L[i][j] M[j][c]
@@ -597,6 +620,7 @@ geninv_status geninv_destroy(geninv_handle h) {
   if (h->upd) cudaStreamDestroy(h->upd);
   if (h->g_factor.exec) cudaGraphExecDestroy(h->g_factor.exec);
   if (h->g_build.exec) cudaGraphExecDestroy(h->g_build.exec);
+  if (h->g_async.exec) cudaGraphExecDestroy(h->g_async.exec);
   for (auto &ev : h->ev_g)
     if (ev) cudaEventDestroy(ev);
   if (h->gstream) cudaStreamDestroy(h->gstream);
@@ -656,6 +680,47 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
   fill_info(info, fs, r, tr, st);
   if (info) info->order = ko ? 1 : 0;
   return st;
+}
+
+geninv_status geninv_d_async(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp,
+                             int64_t ldp, int64_t *rank_dev, const geninv_opts *opts) {
+  if (!h || !Gp || !rank_dev || ldp < m) return GENINV_EINVAL;
+  GI_TRYS(check_g(G, m, n, ld));
+  cudaSetDevice(h->device);
+  const int tr = m < n;
+  const int s = (int)(tr ? m : n);
+  GI_TRYS(ensure_ws(h, s));
+  GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
+  const int np = (s + PB - 1) / PB;
+  const int *rk_final = h->rk + np;
+  const long long key[10] = {s, h->ld, (long long)(uintptr_t)h->A, dbits(tol_rel_of(opts)), dbits(tol_abs_of(opts)),
+                             (long long)(uintptr_t)rank_dev, 3, 0, 0, 0};
+  GI_TRYS(run_graph(h, h->g_async, key, [&](cudaStream_t st) -> geninv_status {
+    cudaStream_t saved = h->st;
+    h->st = st;
+    geninv_status rs = GENINV_OK;
+    do {
+      cudaError_t e = tolerance(h->A, h->ld, s, tol_rel_of(opts), tol_abs_of(opts), h->fs, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(h->L, 0, (size_t)s * h->ld * sizeof(double), st);
+      if (e == cudaSuccess)
+        e = frchol(h->A, h->ld, s, h->L, h->ld, h->piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, st, h->upd, h->ev_fr);
+      if (e == cudaSuccess) {
+        async_pad_kernel<<<(s + 255) / 256, 256, 0, st>>>(h->piv, rk_final, s);
+        e = cudaGetLastError();
+      }
+      if (e != cudaSuccess) { rs = cuda_status(e); break; }
+      h->launches += 2 + np + 2 * std::max(0, np - 2);
+      rs = build_x(h, s, s, true, rk_final);
+      if (rs != GENINV_OK) break;
+      async_rank_kernel<<<1, 1, 0, st>>>(rank_dev, rk_final, h->fs, h->fs2);
+      if ((e = cudaGetLastError()) != cudaSuccess) rs = cuda_status(e);
+      h->launches += 1;
+    } while (0);
+    h->st = saved;
+    return rs;
+  }));
+  h->x_s = s;
+  return apply(h, G, m, n, ld, tr, Gp, ldp, h->st);
 }
 
 geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, int64_t n, int64_t ld, double *Gp_host,
