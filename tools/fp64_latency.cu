@@ -1,38 +1,54 @@
-// Latency of dependent FP64 ops for one warp on sm_100a (measurement tool only).
+// Dependent-chain latency (cycles per op) of the FP64 operations on the panel factor's pivot chain
+// (measurement tool only).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_latency tools/fp64_latency.cu
 #include <cstdio>
 #include <cuda_runtime.h>
-__global__ void lat(double *out, long long *cyc, double x0, int n) {
-  double x = x0 + threadIdx.x * 1e-9, y = 1.000001;
-  long long t0, t1;
-  // DFMA chain
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) x = fma(x, y, 1e-12);
-  t1 = clock64(); if (threadIdx.x == 0) cyc[0] = (t1 - t0) / n;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) x = 1.0 / x + 0.5;
-  t1 = clock64(); if (threadIdx.x == 0) cyc[1] = (t1 - t0) / n;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) x = sqrt(x) + 0.25;
-  t1 = clock64(); if (threadIdx.x == 0) cyc[2] = (t1 - t0) / n;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) x = __shfl_sync(0xffffffffu, x, (threadIdx.x + 1) & 31) * 1.0000001;
-  t1 = clock64(); if (threadIdx.x == 0) cyc[3] = (t1 - t0) / n;
-  __shared__ double sm[64];
-  sm[threadIdx.x] = x; __syncwarp();
-  t0 = clock64();
-  int j = threadIdx.x;
-  for (int i = 0; i < n; ++i) { double v = sm[j]; j = ((int)v & 1) ^ threadIdx.x; sm[threadIdx.x] = v + 1.0; }
-  t1 = clock64(); if (threadIdx.x == 0) cyc[4] = (t1 - t0) / n;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) x = x / y + 1e-3;
-  t1 = clock64(); if (threadIdx.x == 0) cyc[5] = (t1 - t0) / n;
-  out[threadIdx.x] = x + sm[j];
+
+constexpr int N = 256;
+
+template <int OP>
+__global__ void chain(double x0, double *out, long long *cyc) {
+  double x = x0 + threadIdx.x * 1e-3;
+  const double c = 1.0000001, e = 0.9999999;
+  __syncwarp();
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < N; ++i) {
+    if (OP == 0) x = fma(x, c, -1e-9);                             // DFMA
+    if (OP == 1) x = sqrt(x) + 0.5;                                // sqrt (+ DADD)
+    if (OP == 2) x = c / x;                                        // IEEE division
+    if (OP == 3) x = 1.0 / x;                                      // IEEE reciprocal
+    if (OP == 4) x = __shfl_sync(0xffffffffu, x, (threadIdx.x + 1) & 31) * e;  // shfl (+ DMUL)
+    if (OP == 5) x = rsqrt(x) + 0.5;                               // rsqrt (+ DADD)
+    if (OP == 6) x = __drcp_rn(x);                                 // __drcp_rn
+    if (OP == 7) x = x * c;                                        // DMUL
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
+
+template <int OP>
+void run(double *o, long long *c, const char *name, double x0 = 2.0) {
+  chain<OP><<<1, 32>>>(x0, o, c);
+  chain<OP><<<1, 32>>>(x0, o, c);
+  long long h;
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("%-22s %6.1f cycles / op\n", name, (double)h / N);
+}
+
 int main() {
-  double *o; long long *c; cudaMalloc(&o, 256); cudaMalloc(&c, 64);
-  lat<<<1, 32>>>(o, c, 1.5, 1000); cudaDeviceSynchronize();
-  lat<<<1, 32>>>(o, c, 1.5, 10000); cudaDeviceSynchronize();
-  long long h[6]; cudaMemcpy(h, c, 48, cudaMemcpyDeviceToHost);
-  printf("cycles per dependent op: dfma %lld  rcp-div(1/x) %lld  sqrt %lld  shfl+dmul %lld  lds+sts %lld  div(x/y) %lld\n", h[0], h[1], h[2], h[3], h[4], h[5]);
+  double *o;
+  long long *c;
+  cudaMalloc(&o, 32 * 8);
+  cudaMalloc(&c, 8);
+  run<0>(o, c, "dfma");
+  run<7>(o, c, "dmul");
+  run<1>(o, c, "sqrt + dadd");
+  run<2>(o, c, "div");
+  run<3>(o, c, "1.0 / x");
+  run<6>(o, c, "__drcp_rn");
+  run<5>(o, c, "rsqrt + dadd");
+  run<4>(o, c, "shfl + dmul");
   return 0;
 }
