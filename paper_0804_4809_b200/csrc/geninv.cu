@@ -34,7 +34,7 @@ struct geninv_handle_s {
   cudaStream_t gstream = nullptr;   // private non-blocking stream the graphs are captured / launched on
   cudaEvent_t ev_g[2] = {};
   cudaEvent_t ev[4] = {};
-  cudaEvent_t ev_fr[4] = {};  // frchol lookahead events
+  cudaEvent_t ev_fr[6] = {};  // frchol lookahead events
   // s x s workspaces (leading dimension ld >= round_up(s, 32))
   int s_cap = 0;
   long long ld = 0;
@@ -109,7 +109,7 @@ geninv_status ensure_ws(geninv_handle h, int s) {
   const size_t sq = (size_t)ld * ld * sizeof(double);
   double **bufs[] = {&h->A, &h->L, &h->Bm, &h->Cf, &h->Ci, &h->Mm, &h->Kb, &h->X, &h->T};
   for (auto b : bufs) GI_TRY(cudaMalloc(b, sq));
-  h->wp_elems = 18LL * ld * PB;
+  h->wp_elems = 20LL * ld * PB;
   GI_TRY(cudaMalloc(&h->Wp, h->wp_elems * sizeof(double)));
   const int np = (int)(ld / PB) + 2;
   GI_TRY(cudaMalloc(&h->rk, np * sizeof(int)));
@@ -585,7 +585,7 @@ geninv_status geninv_create(geninv_handle *out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->upd, cudaStreamNonBlocking);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming);
-  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_fr[i], cudaEventDisableTiming);
+  for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_fr[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_g[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {

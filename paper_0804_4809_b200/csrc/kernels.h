@@ -24,10 +24,10 @@ cudaError_t tolerance(const double *A, long long lda, int s, double tol_rel, dou
 // a3: blocked left-looking rank-revealing Cholesky with one-panel lookahead.
 // L (s x s, ldl) must be zero on entry; rk: device int[ceil(s/PB)+1] (rk[p] =
 // rank before panel p, rk[npanels] = final rank); piv: device int[s]; Wp:
-// workspace of wp_elems doubles (>= 18 * s * PB).  mode 0: drop iff pivot <=
+// workspace of wp_elems doubles (>= 20 * s * PB).  mode 0: drop iff pivot <=
 // tol (paper); mode 1: SPD (accept iff pivot > 0, flag bit1 otherwise).  The
 // big updates run on `upd` (a second stream) concurrently with the previous
-// panel; ev: 4 events owned by the caller.
+// one or two panels (lookahead depth by s); ev: 5 events owned by the caller.
 cudaError_t frchol(const double *A, long long lda, int s, double *L, long long ldl, int *piv, int *rk,
                    FactorStats *st, int mode, double *Wp, long long wp_elems, cudaStream_t stream,
                    cudaStream_t upd, cudaEvent_t *ev);
