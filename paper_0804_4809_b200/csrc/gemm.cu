@@ -3,6 +3,10 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <array>
+#include <map>
+#include <queue>
+#include <vector>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -106,6 +110,84 @@ static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
   dim3 grid((unsigned)tiles, op.splits, op.batch);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(a);
   return cudaGetLastError();
+}
+
+// Split count (1..max_splits) for a 128 x 128 launch that minimises its simulated duration: the
+// tiles x splits CTAs in launch order, each placed on the SM that frees first (one CTA per SM),
+// cost = per-CTA overhead + its k-slabs, plus the fixed-order reduction's traffic.  Per-tile
+// k-ranges follow GemmArgs (device-side pivots assumed evenly spread, rows ~ j * rows / K).
+static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms);
+
+int balanced_splits(const GemmOp &op, int max_splits, int sms) {
+  if (op.M <= 0 || op.N <= 0 || op.batch != 1 || op.K_dev) return 1;
+  // memoised per shape (the simulation is ~1e4 heap operations; it must not sit on the host path)
+  static std::mutex mu;
+  static std::map<std::array<long long, 9>, int> cache;
+  const std::array<long long, 9> key = {op.M, op.N, op.K, op.lower, op.mirror, op.k_lo_mode, op.k_hi_mode, max_splits,
+                                        sms};
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const int S = balanced_splits_sim(op, max_splits, sms);
+  cache[key] = S;
+  return S;
+}
+
+static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
+  const int mt = (op.M + 127) / 128, nt = (op.N + 127) / 128;
+  const long long nsl = (op.K + BK - 1) / BK;
+  std::vector<int> len;
+  // tile order of the kernel (lower: row-major over the lower triangle; else the banded raster)
+  const long long per_tile = 128LL * (op.K > 0 ? op.K : 1) * 8;
+  const long long mbw = std::max<long long>(1, (48LL << 20) / per_tile);
+  const long long nbands = (mt + mbw - 1) / mbw;
+  const int mband = (int)((mt + nbands - 1) / nbands);
+  const double kpm = (double)op.K / op.M;   // pivots evenly spread: piv[j] ~ j K / M (L'L), #{piv < m} ~ m K / M (L M)
+  auto tile_len = [&](int tm, int tn) {
+    const long long m0 = 128LL * tm, n0 = 128LL * tn;
+    long long klo = 0, khi = nsl;
+    if (op.k_lo_mode == 1) klo = m0 / BK;
+    else if (op.k_lo_mode == 2) klo = n0 / BK;
+    else if (op.k_lo_mode == 3) klo = (long long)(m0 * kpm) / BK;
+    if (op.k_hi_mode == 1) khi = std::min(khi, (m0 + 128 + BK - 1) / BK);
+    if (op.k_hi_mode == 2) khi = std::min(khi, ((long long)((m0 + 128) * kpm) + BK - 1) / BK);
+    return (int)std::max(0LL, khi - std::min(klo, khi));
+  };
+  if (op.lower) {
+    for (int bi = 0; bi < mt; ++bi)
+      for (int bj = 0; bj <= bi; ++bj) len.push_back(tile_len(bi, bj));
+  } else {
+    for (int band = 0; band * mband < mt; ++band) {
+      const int mb = std::min(mband, mt - band * mband);
+      for (int t = 0; t < mb * nt; ++t) len.push_back(tile_len(band * mband + t % mb, t / mb));
+    }
+  }
+  const double over = 1.0;                              // per-CTA prologue + epilogue, in k-slab units
+  const double red_per_elem = 8.0 / 3.0e12 / 2.1e-6;    // slab units per byte of the reduction (~3 TB/s)
+  const double out_elems = op.lower && !op.mirror ? 0.5 * op.M * (op.M + 1.0) : (double)op.M * op.N;
+  double best = 1e300;
+  int bs = 1;
+  for (int S = 1; S <= max_splits; ++S) {
+    std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+    for (int i = 0; i < sms; ++i) q.push(0.0);
+    double span = 0.0;
+    for (int z = 0; z < S; ++z)
+      for (int l : len) {
+        const int per = (l + S - 1) / S;
+        const int mine = std::max(0, std::min(l, per * (z + 1)) - std::min(l, per * z));
+        const double t0 = q.top();
+        q.pop();
+        const double t1 = t0 + over + mine;
+        q.push(t1);
+        span = std::max(span, t1);
+      }
+    const double total = span + (S > 1 ? (S + 1.0) * out_elems * red_per_elem + 2.0 : 0.0);
+    if (total < best * 0.97) {   // a split must win by 3 %
+      best = total;
+      bs = S;
+    }
+  }
+  return bs;
 }
 
 cudaError_t gemm(const GemmOp &op, cudaStream_t st) {

@@ -41,4 +41,7 @@ cudaError_t splitk_reduce(const double *P, long long split_stride, int splits, l
 
 int num_sms();
 
+// Split-K count for a 128 x 128 launch from a schedule simulation (see gemm.cu); 1 = no split.
+int balanced_splits(const GemmOp &op, int max_splits, int sms);
+
 }  // namespace gi

@@ -311,16 +311,25 @@ geninv_status factor(geninv_handle h, const double *A, long long lda, int s, dou
   return GENINV_OK;
 }
 
-// a5: M (r x r, ldm, full symmetric) = inv(B), B SPD (lower, ldb).  No sync.
-geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb, double *M, long long ldm) {
+// ---- the chain GEMMs (a4-a6), built in one place so the split plan can be computed before capture
+GemmOp op_ltl(geninv_handle h, int s, int r) {   // a4: B = L'L (r x r, lower): B[i][j] = sum_k L[k][i] L[k][j]
+  const long long ld = h->ld;
+  GemmOp b;
+  b.A = Mat{h->L, ld, s, ld};
+  b.B = b.A;
+  b.a_kmajor = b.b_kmajor = false;
+  b.M = b.N = r;
+  b.K = s;
+  b.lower = true;
+  b.k_lo_mode = 3;                                     // L[k][i] = 0 above the pivot row piv[i] (Eq. 1)
+  b.k_lo_dev = h->piv;
+  b.C = h->Bm;
+  b.ldc = ld;
+  return b;
+}
+GemmOp op_lauum(geninv_handle h, int r, double *M, long long ldm) {   // M = C^-T C^-1 (full symmetric)
   const long long ld = h->ld;
   const int r_pad = (r + 31) / 32 * 32;
-  GI_TRY(cudaMemsetAsync(h->Cf, 0, (size_t)r_pad * ld * sizeof(double), h->st));
-  GI_TRY(cudaMemsetAsync(h->Ci, 0, (size_t)r_pad * ld * sizeof(double), h->st));
-  GI_TRY(tolerance(B, ldb, r, 0.0, 0.0, h->fs2, h->st));
-  GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st, h->upd, h->ev_fr));
-  GI_TRY(trtri_lower(h->Cf, ld, r, h->Ci, ld, h->T, h->st));
-  // M = C^-T C^-1 : M[i][j] = sum_k Ci[k][i] Ci[k][j]
   GemmOp op;
   op.A = Mat{h->Ci, ld, r_pad, r_pad};
   op.B = op.A;
@@ -332,11 +341,105 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   op.k_lo_mode = 1;                                    // C^-1 lower: Ci[k][i] = 0 for k < i
   op.C = M;
   op.ldc = ldm;
+  return op;
+}
+GemmOp op_k(geninv_handle h, int s, int r) {   // a6: K = L M (s x r):  K[i][c] = sum_j L[i][j] M[j][c]
+  const long long ld = h->ld;
+  GemmOp k;
+  k.A = Mat{h->L, ld, s, r};
+  k.a_kmajor = true;
+  k.B = Mat{h->Mm, ld, r, r};
+  k.b_kmajor = false;
+  k.M = s;
+  k.N = r;
+  k.K = r;
+  k.k_hi_mode = 2;                                     // L[i][j] = 0 for rows i < piv[j] (Eq. 1)
+  k.k_lo_dev = h->piv;
+  k.C = h->Kb;
+  k.ldc = ld;
+  return k;
+}
+GemmOp op_x(geninv_handle h, int s, int r) {   // X = K K' (s x s, full symmetric)
+  const long long ld = h->ld;
+  GemmOp x;
+  x.A = Mat{h->Kb, ld, s, r};
+  x.B = x.A;
+  x.a_kmajor = x.b_kmajor = true;
+  x.M = x.N = s;
+  x.K = r;
+  x.lower = true;
+  x.mirror = true;
+  x.C = h->X;
+  x.ldc = ld;
+  return x;
+}
+
+int chain_splits(const GemmOp &op) {
+  static const int on = [] {
+    const char *e = getenv("GENINV_CHAIN_SPLIT");   // 0 disables (tuning / A-B runs)
+    return e ? atoi(e) : 1;
+  }();
+  return on ? balanced_splits(op, 8, num_sms()) : 1;
+}
+
+// One chain GEMM with the split-K count of its schedule simulation; partial slices in h->part
+// (sized by prepare_chain beforehand: no allocation while a graph is being captured).
+geninv_status gemm_chain(geninv_handle h, GemmOp op) {
+  int S = chain_splits(op);
+  const long long pstride = (long long)op.M * op.N;
+  while (S > 1 && (size_t)S * pstride * sizeof(double) > h->part_bytes) --S;
+  if (getenv("GENINV_DEBUG_SPLITS"))
+    fprintf(stderr, "chain gemm M=%d N=%d K=%d lower=%d lo=%d hi=%d -> splits %d\n", op.M, op.N, op.K, (int)op.lower,
+            op.k_lo_mode, op.k_hi_mode, S);
+  if (S <= 1) {
+    GI_TRY(gemm(op, h->st));
+    h->launches += 1;
+    return GENINV_OK;
+  }
+  double *C = op.C;
+  const long long ldc = op.ldc;
+  const double alpha = op.alpha;
+  const double *C0 = op.C0;
+  const long long ldc0 = op.ldc0;
+  op.C = h->part;
+  op.ldc = op.N;
+  op.C0 = nullptr;
+  op.splits = S;
+  op.split_stride = pstride;
   GI_TRY(gemm(op, h->st));
+  GI_TRY(splitk_reduce(h->part, pstride, S, op.N, C, ldc, C0, ldc0, alpha, op.M, op.N, op.lower && !op.mirror,
+                       h->st));
+  h->launches += 2;
+  return GENINV_OK;
+}
+
+// Size h->part for the chain GEMMs of (s, r) before the chain is captured.
+geninv_status prepare_chain(geninv_handle h, int s, int r, bool want_x) {
+  if (r == 0) return GENINV_OK;
+  size_t need = 0;
+  GemmOp ops[4] = {op_ltl(h, s, r), op_lauum(h, r, h->Mm, h->ld), op_k(h, s, r), op_x(h, s, r)};
+  for (int i = 0; i < (want_x ? 4 : 3); ++i) {
+    const int S = chain_splits(ops[i]);
+    if (S > 1) need = std::max(need, (size_t)S * ops[i].M * ops[i].N * sizeof(double));
+  }
+  return ensure_part(h, need);
+}
+
+// a5: M (r x r, ldm, full symmetric) = inv(B), B SPD (lower, ldb).  No sync.
+geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb, double *M, long long ldm) {
+  const long long ld = h->ld;
+  const int r_pad = (r + 31) / 32 * 32;
+  GI_TRY(cudaMemsetAsync(h->Cf, 0, (size_t)r_pad * ld * sizeof(double), h->st));
+  GI_TRY(cudaMemsetAsync(h->Ci, 0, (size_t)r_pad * ld * sizeof(double), h->st));
+  GI_TRY(tolerance(B, ldb, r, 0.0, 0.0, h->fs2, h->st));
+  GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st, h->upd, h->ev_fr));
+  GI_TRY(trtri_lower(h->Cf, ld, r, h->Ci, ld, h->T, h->st));
+  // M = C^-T C^-1 : M[i][j] = sum_k Ci[k][i] Ci[k][j]
+  GI_TRYS(gemm_chain(h, op_lauum(h, r, M, ldm)));
   const int np = (r + PB - 1) / PB;
   int lev = 0;
   for (int hh = 32; hh < r_pad; hh *= 2) ++lev;
-  h->launches += 1 + np + 2 * std::max(0, np - 2) + 2 + 4 * lev + 1;
+  h->launches += 1 + np + 2 * std::max(0, np - 2) + 2 + 4 * lev;
   return GENINV_OK;
 }
 
@@ -365,20 +468,7 @@ geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true, const i
     GI_TRY(cudaMemsetAsync(h->X, 0, (size_t)s * ld * sizeof(double), h->st));
     return GENINV_OK;
   }
-  // a4: B = L'L (r x r, lower): B[i][j] = sum_k L[k][i] L[k][j]
-  GemmOp b;
-  b.A = Mat{h->L, ld, s, ld};
-  b.B = b.A;
-  b.a_kmajor = b.b_kmajor = false;
-  b.M = b.N = r;
-  b.K = s;
-  b.lower = true;
-  b.k_lo_mode = 3;                                     // L[k][i] = 0 above the pivot row piv[i] (Eq. 1)
-  b.k_lo_dev = h->piv;
-  b.C = h->Bm;
-  b.ldc = ld;
-  GI_TRY(gemm(b, h->st));
-  h->launches += 1;
+  GI_TRYS(gemm_chain(h, op_ltl(h, s, r)));
   if (rk_pad) {
     identity_tail_kernel<<<(s + 255) / 256, 256, 0, h->st>>>(h->Bm, ld, rk_pad, s);
     GI_TRY(cudaGetLastError());
@@ -386,35 +476,9 @@ geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true, const i
   }
   // a5
   GI_TRYS(spd_inverse(h, h->Bm, r, ld, h->Mm, ld));
-  // a6: K = L M (s x r):  K[i][c] = sum_j L[i][j] M[j][c]
-  GemmOp k;
-  k.A = Mat{h->L, ld, s, r};
-  k.a_kmajor = true;
-  k.B = Mat{h->Mm, ld, r, r};
-  k.b_kmajor = false;
-  k.M = s;
-  k.N = r;
-  k.K = r;
-  k.k_hi_mode = 2;                                     // L[i][j] = 0 for rows i < piv[j] (Eq. 1)
-  k.k_lo_dev = h->piv;
-  k.C = h->Kb;
-  k.ldc = ld;
-  GI_TRY(gemm(k, h->st));
-  h->launches += 1;
+  GI_TRYS(gemm_chain(h, op_k(h, s, r)));
   if (!want_x) return GENINV_OK;
-  // X = K K' (s x s, full symmetric)
-  GemmOp x;
-  x.A = Mat{h->Kb, ld, s, r};
-  x.B = x.A;
-  x.a_kmajor = x.b_kmajor = true;
-  x.M = x.N = s;
-  x.K = r;
-  x.lower = true;
-  x.mirror = true;
-  x.C = h->X;
-  x.ldc = ld;
-  GI_TRY(gemm(x, h->st));
-  h->launches += 1;
+  GI_TRYS(gemm_chain(h, op_x(h, s, r)));
   return GENINV_OK;
 }
 
@@ -530,7 +594,9 @@ geninv_status from_gram(geninv_handle h, const double *A, int s, long long lda, 
   const bool ko = ell > 0 && k_order && k_order_cheaper(s, ell, r);
   if (k_order) *k_order = ko;
   // a4-a6 (L'L, the SPD inverse's panel chain, TRTRI, the products) as one CUDA graph per (s, r)
-  const long long key[10] = {s, r, ko ? 0 : 1, h->ld, (long long)(uintptr_t)h->L, 2, 0, 0, 0, 0};
+  GI_TRYS(prepare_chain(h, s, r, !ko));
+  const long long key[10] = {s, r, ko ? 0 : 1, h->ld, (long long)(uintptr_t)h->L, 2, (long long)(uintptr_t)h->part,
+                             0, 0, 0};
   GI_TRYS(run_graph(h, h->g_build, key, [&](cudaStream_t st) -> geninv_status {
     cudaStream_t saved = h->st;
     h->st = st;
@@ -693,8 +759,9 @@ geninv_status geninv_d_async(geninv_handle h, const double *G, int64_t m, int64_
   GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
   const int np = (s + PB - 1) / PB;
   const int *rk_final = h->rk + np;
+  GI_TRYS(prepare_chain(h, s, s, true));
   const long long key[10] = {s, h->ld, (long long)(uintptr_t)h->A, dbits(tol_rel_of(opts)), dbits(tol_abs_of(opts)),
-                             (long long)(uintptr_t)rank_dev, 3, 0, 0, 0};
+                             (long long)(uintptr_t)rank_dev, 3, (long long)(uintptr_t)h->part, 0, 0};
   GI_TRYS(run_graph(h, h->g_async, key, [&](cudaStream_t st) -> geninv_status {
     cudaStream_t saved = h->st;
     h->st = st;
@@ -1038,6 +1105,11 @@ geninv_status geninv_spd_inverse_d(geninv_handle h, const double *B, int64_t r, 
   if (!h || !B || !M || r < 1 || ldb < r || ldm < r) return GENINV_EINVAL;
   cudaSetDevice(h->device);
   GI_TRYS(ensure_ws(h, (int)r));
+  {
+    const GemmOp o = op_lauum(h, (int)r, M, ldm);
+    const int S = chain_splits(o);
+    if (S > 1) GI_TRYS(ensure_part(h, (size_t)S * o.M * o.N * sizeof(double)));
+  }
   GI_TRYS(spd_inverse(h, B, (int)r, ldb, M, ldm));
   return finish_spd_check(h, (int)r);
 }

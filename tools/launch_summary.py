@@ -1,37 +1,38 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum CSV launch list: time share per kernel."""
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv): total and per kernel/grid.
+
+    python tools/launch_summary.py launches.csv [top]
+"""
 import collections
 import csv
-import io
 import sys
 
-
-def load(path):
-    txt = open(path).read().splitlines()
-    start = next(i for i, l in enumerate(txt) if l.startswith('"ID"'))
-    return list(csv.DictReader(io.StringIO("\n".join(txt[start:]))))
+UNIT = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 
 
-def summarise(path, top=30):
-    rows = load(path)
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    unit = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
+def main():
+    path = sys.argv[1]
+    top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    rows = [r for r in csv.DictReader(line for line in open(path) if not line.startswith("=="))
+            if r.get("Metric Name") == "gpu__time_duration.sum"]
+    agg = collections.OrderedDict()
+    tot = 0.0
     for r in rows:
-        if r["Metric Name"] != "gpu__time_duration.sum":
-            continue
+        v = float(r["Metric Value"].replace(",", "")) * UNIT[r["Metric Unit"]]
         name = r["Kernel Name"]
-        if "dgemm_tc" in name:
-            key = name[name.index("dgemm_tc"):name.index(">") + 1] + " grid" + r["Grid Size"]
+        if "frchol_panel" in name:
+            k = "frchol_panel_kernel"
+        elif "dgemm_tc<128, 32" in name:
+            k = "dgemm_tc 128x32 (panel update)"
         else:
-            key = name.split("(")[0][-80:]
-        v = float(r["Metric Value"].replace(",", "")) * unit[r["Metric Unit"]]
-        agg[key][0] += 1
-        agg[key][1] += v
-    tot = sum(v[1] for v in agg.values())
-    out = [f"total {tot:.2f} ms over {sum(v[0] for v in agg.values())} launches"]
-    for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
-        out.append(f"{v[1]:12.3f} ms {100 * v[1] / tot:6.2f}%  n={v[0]:5d}  {k}")
-    return "\n".join(out)
+            k = name.split("(")[0][:48] + " grid" + r.get("Grid Size", "")
+        a = agg.setdefault(k, [0.0, 0])
+        a[0] += v
+        a[1] += 1
+        tot += v
+    print(f"total {tot:.1f} us over {len(rows)} launches (serialised, cold L2)")
+    for k, (v, n) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+        print(f"{v:10.1f} us {100 * v / tot:5.1f}%  n={n:4d}  {k}")
 
 
 if __name__ == "__main__":
-    print(summarise(sys.argv[1]))
+    main()
