@@ -119,12 +119,12 @@ static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
 static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms);
 
 int balanced_splits(const GemmOp &op, int max_splits, int sms) {
-  if (op.M <= 0 || op.N <= 0 || op.batch != 1 || op.K_dev) return 1;
+  if (op.M <= 0 || op.N <= 0 || op.batch < 1 || op.K_dev) return 1;
   // memoised per shape (the simulation is ~1e4 heap operations; it must not sit on the host path)
   static std::mutex mu;
-  static std::map<std::array<long long, 9>, int> cache;
-  const std::array<long long, 9> key = {op.M, op.N, op.K, op.lower, op.mirror, op.k_lo_mode, op.k_hi_mode, max_splits,
-                                        sms};
+  static std::map<std::array<long long, 10>, int> cache;
+  const std::array<long long, 10> key = {op.M, op.N, op.K, op.lower, op.mirror, op.k_lo_mode, op.k_hi_mode, max_splits,
+                                         sms, op.batch};
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -171,6 +171,7 @@ static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
     std::priority_queue<double, std::vector<double>, std::greater<double>> q;
     for (int i = 0; i < sms; ++i) q.push(0.0);
     double span = 0.0;
+    for (int b = 0; b < op.batch; ++b)
     for (int z = 0; z < S; ++z)
       for (int l : len) {
         const int per = (l + S - 1) / S;
@@ -181,7 +182,7 @@ static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
         q.push(t1);
         span = std::max(span, t1);
       }
-    const double total = span + (S > 1 ? (S + 1.0) * out_elems * red_per_elem + 2.0 : 0.0);
+    const double total = span + (S > 1 ? (S + 1.0) * out_elems * op.batch * red_per_elem + 2.0 : 0.0);
     if (total < best * 0.97) {   // a split must win by 3 %
       best = total;
       bs = S;

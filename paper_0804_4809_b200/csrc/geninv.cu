@@ -422,6 +422,7 @@ geninv_status prepare_chain(geninv_handle h, int s, int r, bool want_x) {
     const int S = chain_splits(ops[i]);
     if (S > 1) need = std::max(need, (size_t)S * ops[i].M * ops[i].N * sizeof(double));
   }
+  need = std::max(need, (size_t)trtri_part_elems(r, h->ld, h->ld) * sizeof(double));
   return ensure_part(h, need);
 }
 
@@ -433,7 +434,7 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   GI_TRY(cudaMemsetAsync(h->Ci, 0, (size_t)r_pad * ld * sizeof(double), h->st));
   GI_TRY(tolerance(B, ldb, r, 0.0, 0.0, h->fs2, h->st));
   GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st, h->upd, h->ev_fr));
-  GI_TRY(trtri_lower(h->Cf, ld, r, h->Ci, ld, h->T, h->st));
+  GI_TRY(trtri_lower(h->Cf, ld, r, h->Ci, ld, h->T, h->part, (long long)(h->part_bytes / sizeof(double)), h->st));
   // M = C^-T C^-1 : M[i][j] = sum_k Ci[k][i] Ci[k][j]
   GI_TRYS(gemm_chain(h, op_lauum(h, r, M, ldm)));
   const int np = (r + PB - 1) / PB;
@@ -1108,7 +1109,9 @@ geninv_status geninv_spd_inverse_d(geninv_handle h, const double *B, int64_t r, 
   {
     const GemmOp o = op_lauum(h, (int)r, M, ldm);
     const int S = chain_splits(o);
-    if (S > 1) GI_TRYS(ensure_part(h, (size_t)S * o.M * o.N * sizeof(double)));
+    size_t need = S > 1 ? (size_t)S * o.M * o.N * sizeof(double) : 0;
+    need = std::max(need, (size_t)trtri_part_elems((int)r, h->ld, h->ld) * sizeof(double));
+    GI_TRYS(ensure_part(h, need));
   }
   GI_TRYS(spd_inverse(h, B, (int)r, ldb, M, ldm));
   return finish_spd_check(h, (int)r);

@@ -36,8 +36,10 @@ cudaError_t frchol(const double *A, long long lda, int s, double *L, long long l
 // r_pad = round_up(r, 32) with an identity block; C and Cinv are r_pad x r_pad
 // buffers (ld), C zero outside its r x r lower triangle, Cinv zero on entry.
 // T: workspace of r_pad * r_pad doubles.
-cudaError_t trtri_lower(double *C, long long ldc, int r, double *Cinv, long long ldi, double *T,
-                        cudaStream_t stream);
+cudaError_t trtri_lower(double *C, long long ldc, int r, double *Cinv, long long ldi, double *T, double *part,
+                        long long part_elems, cudaStream_t stream);
+// Doubles of split-K partial workspace trtri_lower uses for (r, ldc, ldi) (0: no split).
+long long trtri_part_elems(int r, long long ldc, long long ldi);
 
 // a9: batched small geninv, one CTA per matrix (min(m,n) <= 64, max(m,n) <= 128).  rank[b] >= 0, or
 // -2 (non-finite G) / -3 (L'L not SPD) with G+_b = NaN.  stats (optional, device, one per matrix):

@@ -11,6 +11,11 @@
 #include "gemm_host.h"
 #include "kernels.h"
 
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
+
 namespace gi {
 
 __global__ void pad_identity_kernel(double *C, long long ldc, int r, int r_pad) {
@@ -46,13 +51,10 @@ __global__ void trtri_diag_kernel(const double *__restrict__ C, long long ldc, d
     if (i >= j) Ci[(long long)(b0 + i) * ldi + b0 + j] = x[i];
 }
 
-cudaError_t trtri_lower(double *C, long long ldc, int r, double *Ci, long long ldi, double *T, cudaStream_t st) {
+// The level GEMMs of the recursive doubling, in launch order (op1, op2 per group and level).
+std::vector<GemmOp> trtri_ops(double *C, long long ldc, int r, double *Ci, long long ldi, double *T) {
+  std::vector<GemmOp> ops;
   const int r_pad = (r + 31) / 32 * 32;
-  if (r_pad == 0) return cudaSuccess;
-  if (r_pad > r) pad_identity_kernel<<<1, 32, 0, st>>>(C, ldc, r, r_pad);
-  trtri_diag_kernel<<<r_pad / 32, 32, 0, st>>>(C, ldc, Ci, ldi);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
   for (int h = 32; h < r_pad; h *= 2) {
     // pairs p: block1 rows/cols [2ph, 2ph+h), block2 [(2p+1)h, (2p+1)h + h2)
     const int nfull = r_pad / (2 * h);                 // pairs with h2 == h
@@ -80,8 +82,7 @@ cudaError_t trtri_lower(double *C, long long ldc, int r, double *Ci, long long l
       op1.K = h;
       op1.batch = gr.count;
       op1.k_lo_mode = 2;                               // Cinv11 lower: B(k, n) = 0 for k < n
-      e = gemm(op1, st);
-      if (e != cudaSuccess) return e;
+      ops.push_back(op1);
       // Cinv21 = -Cinv22 * T1   (h2 x h)
       GemmOp op2;
       op2.A = Mat{Ci + (off1 + h) * ldi + off1 + h, ldi, gr.h2, gr.h2, gr.count, bstr_i};
@@ -97,9 +98,76 @@ cudaError_t trtri_lower(double *C, long long ldc, int r, double *Ci, long long l
       op2.K = gr.h2;
       op2.batch = gr.count;
       op2.k_hi_mode = 1;                               // Cinv22 lower: A(m, k) = 0 for k > m
-      e = gemm(op2, st);
-      if (e != cudaSuccess) return e;
+      ops.push_back(op2);
     }
+  }
+  return ops;
+}
+
+int trtri_splits(const GemmOp &op) {
+  static const int on = [] {
+    const char *e = getenv("GENINV_CHAIN_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  return on ? balanced_splits(op, 8, num_sms()) : 1;
+}
+
+long long trtri_part_elems(int r, long long ldc, long long ldi) {
+  long long need = 0;
+  for (const GemmOp &op : trtri_ops(nullptr, ldc, r, nullptr, ldi, nullptr)) {
+    const int S = trtri_splits(op);
+    if (S > 1) need = std::max(need, (long long)S * op.batch * op.M * op.N);
+  }
+  return need;
+}
+
+// Batched fixed-order split-K sum: out_b = alpha * sum_z P[z][b]  (P: split stride sstride, batch stride
+// M * N, ld N; out: batch stride obs, ld ldo).
+__global__ void splitk_reduce_batched_kernel(const double *__restrict__ P, long long sstride, int splits,
+                                             double *__restrict__ out, long long ldo, long long obs, double alpha,
+                                             int M, int N, int batch) {
+  const long long per = (long long)M * N, total = per * batch;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(idx / per);
+    const long long e = idx - b * per;
+    const int i = (int)(e / N), j = (int)(e % N);
+    double v = 0.0;
+    for (int z = 0; z < splits; ++z) v += P[z * sstride + idx];
+    out[b * obs + (long long)i * ldo + j] = alpha * v;
+  }
+}
+
+cudaError_t trtri_lower(double *C, long long ldc, int r, double *Ci, long long ldi, double *T, double *part,
+                        long long part_elems, cudaStream_t st) {
+  const int r_pad = (r + 31) / 32 * 32;
+  if (r_pad == 0) return cudaSuccess;
+  if (r_pad > r) pad_identity_kernel<<<1, 32, 0, st>>>(C, ldc, r, r_pad);
+  trtri_diag_kernel<<<r_pad / 32, 32, 0, st>>>(C, ldc, Ci, ldi);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  for (GemmOp op : trtri_ops(C, ldc, r, Ci, ldi, T)) {
+    int S = part ? trtri_splits(op) : 1;
+    const long long per = (long long)op.M * op.N;
+    while (S > 1 && (long long)S * op.batch * per > part_elems) --S;
+    if (S <= 1) {
+      if ((e = gemm(op, st)) != cudaSuccess) return e;
+      continue;
+    }
+    double *out = op.C;
+    const long long ldo = op.ldc, obs = op.c_bstride;
+    const double alpha = op.alpha;
+    op.C = part;
+    op.ldc = op.N;
+    op.c_bstride = per;
+    op.splits = S;
+    op.split_stride = per * op.batch;
+    if ((e = gemm(op, st)) != cudaSuccess) return e;
+    const long long total = per * op.batch;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 8);
+    splitk_reduce_batched_kernel<<<blocks, 256, 0, st>>>(part, per * op.batch, S, out, ldo, obs, alpha, op.M, op.N,
+                                                         op.batch);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
