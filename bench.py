@@ -91,6 +91,10 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + 3.0                  # the sampler is running before the region starts
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.n0 = len(self.lines)
         except Exception:
             self.proc = None
         return self
@@ -101,6 +105,17 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            n_in = len(self.lines) - getattr(self, "n0", 0)
+            if n_in < 1:                               # region shorter than the 200 ms period: one more
+                try:                                   # sample right at its end (clocks still at load)
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=10).stdout.strip()
+                    if out:
+                        self.lines.append(out.splitlines()[-1])
+                        self.short = True
+                except Exception:
+                    pass
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -110,7 +125,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[max(0, getattr(self, "n0", 0) - 1):]:   # from the last sample before the region
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -124,7 +139,10 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if getattr(self, "short", False):
+            out["note"] = "timed region shorter than the 200 ms sampling period: samples at its start and end"
+        return out
 
 
 # --------------------------------------------------------------------------- distributed
@@ -195,8 +213,8 @@ def oracle_sample(cfg, transposed_of_c3):
         G = G.T[:cols] if transposed_of_c3 else G[:, :cols].copy()
         return np.ascontiguousarray(G), f"{cols} of 16384 long-side lines of C3"
     if cfg.name == "C5":
-        G = I.make_batch(cfg, seed_of(cfg), 0, 512).numpy()
-        return G, "matrices 0..511 of the 65536-matrix batch"
+        G = I.make_batch(cfg, seed_of(cfg), 0, 4096).numpy()
+        return G, "matrices 0..4095 of the 65536-matrix batch"
     G = I.make_single(cfg, seed_of(cfg)).numpy()
     return G, "the whole matrix"
 
@@ -350,6 +368,11 @@ def main():
     F = f_alg(s, ell, piv)
     for _ in range(max(0, args.warmup - 1)):
         step()
+    # inputs (G and G+) that fit in the 126 MB L2 are flushed between timed steps by writing a 512 MB
+    # buffer; the step time is then the sum of per-step event pairs, the flushes outside them
+    flush = (m * n * 8 * 2 < 512e6)
+    fbuf = torch.empty(64 << 20, dtype=torch.float64, device=dev) if flush else None
+    step_ev = []
     barrier(world)
     l0 = h.launch_count
     with ClockSampler(local) as clk:
@@ -357,20 +380,55 @@ def main():
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
-            info = step(record=True)
+            if flush:
+                fbuf.fill_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                info = step(record=True)
+                b.record(stream)
+                step_ev.append((a, b))
+            else:
+                info = step(record=True)
         t1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
     launches = (h.launch_count - l0) * world + (args.steps * world if world > 1 else 0)  # + NCCL all-reduce
-    ms = t0.elapsed_time(t1) / args.steps
+    if flush:
+        ms = float(sum(a.elapsed_time(b) for a, b in step_ev)) / args.steps
+    else:
+        ms = t0.elapsed_time(t1) / args.steps
     ms = allmax(ms, world)
     value = F["total"] / (ms * 1e-3) / 1e9
     peak, peak_src = fp64_peak()
-    # dominant kernel: a7 output product, one launch per step per rank
+    # dominant kernel: a7 output product, one launch per step per rank.  Whole-call configs (the a7
+    # launch is inside geninv_d) time the same launch through geninv_apply_d right after the timed
+    # region: K launches on the same X and G, each between CUDA events on the launching stream
+    roof_note = "a7 launches of the timed steps (CUDA events around each on the launching stream)"
+    if whole:
+        Gp_ap = torch.empty(n, m, dtype=torch.float64, device=dev)
+        try:
+            for _ in range(args.steps):
+                if flush:
+                    fbuf.fill_(1.0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                h.geninv_apply_d(G, tr, Gp_ap)
+                e1.record(stream)
+                ev_out.append((e0, e1))
+            torch.cuda.synchronize()
+            roof_note = ("geninv_apply_d (the same a7 launch geninv_d makes, on the X the timed calls left) x "
+                         "steps after the timed region, CUDA events around each")
+        except Exception as exc:   # the one-CTA small path (C1) keeps no X: its kernel is the batched one
+            ev_out.clear()
+            roof_note = f"not separable: {str(exc)[:120]}"
+        del Gp_ap
     if ev_out:
         out_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_out]))
         out_ms = allmax(out_ms, world)
-        out_flops_launch = 2.0 * s * s * rows
+        out_flops_launch = 2.0 * s * s * (rows if not whole else ell)
+        if info is not None and getattr(info, "order", 0) == 1:   # low-rank K order: K (K'G'), 4 r s ell
+            out_flops_launch = 4.0 * info.rank * s * (rows if not whole else ell)
         achieved = out_flops_launch / (out_ms * 1e-3) / 1e12
     else:
         out_ms, achieved, out_flops_launch = None, None, None
@@ -422,8 +480,9 @@ def main():
                        "phase_ms_rank0": phases,
                        "flops_breakdown": {k: v for k, v in F.items() if k != "total"},
                        "l2": "inputs (G 64 GiB) far larger than the 126 MB L2; no flush needed"
-                       if cfg.name == "C4" else "inputs larger than L2" if m * n * 8 > 126e6 else
-                       "inputs smaller than L2 (not flushed)"},
+                       if cfg.name == "C4" else ("L2 flushed before every timed step (512 MB write); step time = "
+                                                 "sum of per-step CUDA event pairs") if flush else
+                       "inputs (G + G+) larger than 512 MB, 4x the L2; no flush needed"},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -431,7 +490,7 @@ def main():
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "dgemm_tc<128,128,64,32,6,K-major,K-major> (a7 G+ = X G')",
                          "flops_per_launch": out_flops_launch, "ms_per_launch": out_ms,
-                         "peak_source": peak_src},
+                         "measured": roof_note, "peak_source": peak_src},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -515,6 +574,53 @@ def bench_batched(args, cfg, desc, world, rank):
     F = sum(f_alg(s, ell, np.arange(int(r)))["total"] for r in ranks) * world
     peak, src = fp64_peak()
     value = F / (ms * 1e-3) / 1e9
+    # e2e: every step copies this rank's G from pinned host memory, runs geninv_batched_d and reads G+ and
+    # the ranks back into pinned host memory (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        Gh = torch.empty(G.shape, dtype=torch.float64).pin_memory()
+        Gh.copy_(G)
+        Gph = torch.empty(Gp.shape, dtype=torch.float64).pin_memory()
+        rkh = torch.empty(rk.shape, dtype=torch.int32).pin_memory()
+        torch.cuda.synchronize()
+        barrier(world)
+        # 8 chunks round-robin over 3 streams: the H2D copy of one chunk, the kernel of another and the
+        # D2H copy of a third overlap (PCIe is full duplex)
+        nch, streams = 8, [torch.cuda.Stream(dev) for _ in range(3)]
+        bounds = [nb * c // nch for c in range(nch + 1)]
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for st_ in streams:
+            st_.wait_event(a0)
+        for _ in range(args.steps):
+            for c in range(nch):
+                lo, hi = bounds[c], bounds[c + 1]
+                st_ = streams[c % 3]
+                with torch.cuda.stream(st_):
+                    G[lo:hi].copy_(Gh[lo:hi], non_blocking=True)
+                    h.use_stream(st_)
+                    h.geninv_batched_d(G[lo:hi], Gp[lo:hi], rk[lo:hi])
+                    Gph[lo:hi].copy_(Gp[lo:hi], non_blocking=True)
+                    rkh[lo:hi].copy_(rk[lo:hi], non_blocking=True)
+        for st_ in streams:
+            stream.wait_stream(st_)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        h.use_stream(stream)
+        ems = allmax(a0.elapsed_time(a1) / args.steps, world)
+        e2e = {"value": F / (ems * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(Gh.numel() * 8) * world,
+               "d2h_bytes_per_step": int(Gph.numel() * 8 + rkh.numel() * 4) * world,
+               "api": "geninv_batched_d on 8 batch chunks over 3 streams, pinned host G / G+ / rank copies"}
+        del Gh, Gph, rkh
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Gs, sample = oracle_sample(cfg, False)
+        fl, dt = run_oracle_once(Gs)
+        fl, dt = run_oracle_once(Gs)
+        cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": sample + f"; oracle = numpy batched geninv (P:105-140 per matrix), {dt:.2f} s"}
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -523,8 +629,11 @@ def bench_batched(args, cfg, desc, world, rank):
                           "config": {"workload": desc, "batch": cfg.batch, "us_per_matrix": ms * 1e3 / cfg.batch,
                                      "hbm_gbs": 2 * cfg.batch * cfg.m * cfg.n * 8 / (ms * 1e-3) / 1e9},
                           "clocks": clk.summary(),
+                          "e2e": e2e,
                           "roofline": {"bound": "tensor", "achieved": value / 1e3, "peak": peak, "unit": "TFLOP/s",
-                                       "frac": value / 1e3 / peak, "traffic": None, "peak_source": src},
+                                       "frac": value / 1e3 / peak, "traffic": None, "peak_source": src,
+                                       "kernel": "batched_geninv_kernel (one launch per step: the whole path)"},
+                          "cpu_baseline": cpu,
                           "gpu_launches": args.steps}), flush=True)
     return 0
 
