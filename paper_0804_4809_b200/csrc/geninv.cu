@@ -24,7 +24,7 @@ using namespace gi;
 
 struct geninv_handle_s {
   int device = 0;
-  cudaStream_t own = nullptr, st = nullptr, st2 = nullptr, upd = nullptr;
+  cudaStream_t own = nullptr, st = nullptr, st2 = nullptr, upd = nullptr, upd2 = nullptr;
   // CUDA graphs of the launch-bound factorisation chain (replayed while the shapes/pointers match)
   struct GraphSlot {
     cudaGraphExec_t exec = nullptr;
@@ -34,7 +34,7 @@ struct geninv_handle_s {
   cudaStream_t gstream = nullptr;   // private non-blocking stream the graphs are captured / launched on
   cudaEvent_t ev_g[2] = {};
   cudaEvent_t ev[4] = {};
-  cudaEvent_t ev_fr[6] = {};  // frchol lookahead events
+  cudaEvent_t ev_fr[8] = {};  // frchol lookahead events
   // s x s workspaces (leading dimension ld >= round_up(s, 32))
   int s_cap = 0;
   long long ld = 0;
@@ -109,7 +109,7 @@ geninv_status ensure_ws(geninv_handle h, int s) {
   const size_t sq = (size_t)ld * ld * sizeof(double);
   double **bufs[] = {&h->A, &h->L, &h->Bm, &h->Cf, &h->Ci, &h->Mm, &h->Kb, &h->X, &h->T};
   for (auto b : bufs) GI_TRY(cudaMalloc(b, sq));
-  h->wp_elems = 20LL * ld * PB;
+  h->wp_elems = 40LL * ld * PB;
   GI_TRY(cudaMalloc(&h->Wp, h->wp_elems * sizeof(double)));
   const int np = (int)(ld / PB) + 2;
   GI_TRY(cudaMalloc(&h->rk, np * sizeof(int)));
@@ -297,11 +297,11 @@ geninv_status factor(geninv_handle h, const double *A, long long lda, int s, dou
   GI_TRYS(run_graph(h, h->g_factor, key, [&](cudaStream_t st) -> geninv_status {
     GI_TRY(tolerance(A, lda, s, tol_rel_of(opts), tol_abs_of(opts), h->fs, st));
     GI_TRY(cudaMemsetAsync(L, 0, (size_t)s * ldl * sizeof(double), st));
-    GI_TRY(frchol(A, lda, s, L, ldl, piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, st, h->upd, h->ev_fr));
+    GI_TRY(frchol(A, lda, s, L, ldl, piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, st, h->upd, h->upd2, h->ev_fr));
     return GENINV_OK;
   }));
   const int np = (s + PB - 1) / PB;
-  h->launches += 1 + np + 2 * std::max(0, np - 2);
+  h->launches += 1 + frchol_launches(s);
   int r = 0;
   GI_TRY(cudaMemcpyAsync(&r, h->rk + np, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   GI_TRY(cudaMemcpyAsync(hst, h->fs, sizeof(FactorStats), cudaMemcpyDeviceToHost, h->st));
@@ -433,14 +433,11 @@ geninv_status spd_inverse(geninv_handle h, const double *B, int r, long long ldb
   GI_TRY(cudaMemsetAsync(h->Cf, 0, (size_t)r_pad * ld * sizeof(double), h->st));
   GI_TRY(cudaMemsetAsync(h->Ci, 0, (size_t)r_pad * ld * sizeof(double), h->st));
   GI_TRY(tolerance(B, ldb, r, 0.0, 0.0, h->fs2, h->st));
-  GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st, h->upd, h->ev_fr));
+  GI_TRY(frchol(B, ldb, r, h->Cf, ld, h->piv2, h->rk2, h->fs2, 1, h->Wp, h->wp_elems, h->st, h->upd, h->upd2, h->ev_fr));
   GI_TRY(trtri_lower(h->Cf, ld, r, h->Ci, ld, h->T, h->part, (long long)(h->part_bytes / sizeof(double)), h->st));
   // M = C^-T C^-1 : M[i][j] = sum_k Ci[k][i] Ci[k][j]
   GI_TRYS(gemm_chain(h, op_lauum(h, r, M, ldm)));
-  const int np = (r + PB - 1) / PB;
-  int lev = 0;
-  for (int hh = 32; hh < r_pad; hh *= 2) ++lev;
-  h->launches += 1 + np + 2 * std::max(0, np - 2) + 2 + 4 * lev;
+  h->launches += 1 + frchol_launches(r) + trtri_launches(r, ld, ld, (long long)(h->part_bytes / sizeof(double)));
   return GENINV_OK;
 }
 
@@ -651,8 +648,9 @@ geninv_status geninv_create(geninv_handle *out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->upd, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->upd2, cudaStreamNonBlocking);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming);
-  for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_fr[i], cudaEventDisableTiming);
+  for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_fr[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&h->ev_g[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -685,6 +683,7 @@ geninv_status geninv_destroy(geninv_handle h) {
   for (auto &ev : h->ev_fr)
     if (ev) cudaEventDestroy(ev);
   if (h->upd) cudaStreamDestroy(h->upd);
+  if (h->upd2) cudaStreamDestroy(h->upd2);
   if (h->g_factor.exec) cudaGraphExecDestroy(h->g_factor.exec);
   if (h->g_build.exec) cudaGraphExecDestroy(h->g_build.exec);
   if (h->g_async.exec) cudaGraphExecDestroy(h->g_async.exec);
@@ -771,13 +770,13 @@ geninv_status geninv_d_async(geninv_handle h, const double *G, int64_t m, int64_
       cudaError_t e = tolerance(h->A, h->ld, s, tol_rel_of(opts), tol_abs_of(opts), h->fs, st);
       if (e == cudaSuccess) e = cudaMemsetAsync(h->L, 0, (size_t)s * h->ld * sizeof(double), st);
       if (e == cudaSuccess)
-        e = frchol(h->A, h->ld, s, h->L, h->ld, h->piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, st, h->upd, h->ev_fr);
+        e = frchol(h->A, h->ld, s, h->L, h->ld, h->piv, h->rk, h->fs, 0, h->Wp, h->wp_elems, st, h->upd, h->upd2, h->ev_fr);
       if (e == cudaSuccess) {
         async_pad_kernel<<<(s + 255) / 256, 256, 0, st>>>(h->piv, rk_final, s);
         e = cudaGetLastError();
       }
       if (e != cudaSuccess) { rs = cuda_status(e); break; }
-      h->launches += 2 + np + 2 * std::max(0, np - 2);
+      h->launches += 2 + frchol_launches(s);
       rs = build_x(h, s, s, true, rk_final);
       if (rs != GENINV_OK) break;
       async_rank_kernel<<<1, 1, 0, st>>>(rank_dev, rk_final, h->fs, h->fs2);

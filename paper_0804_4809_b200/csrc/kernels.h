@@ -24,13 +24,17 @@ cudaError_t tolerance(const double *A, long long lda, int s, double tol_rel, dou
 // a3: blocked left-looking rank-revealing Cholesky with one-panel lookahead.
 // L (s x s, ldl) must be zero on entry; rk: device int[ceil(s/PB)+1] (rk[p] =
 // rank before panel p, rk[npanels] = final rank); piv: device int[s]; Wp:
-// workspace of wp_elems doubles (>= 20 * s * PB).  mode 0: drop iff pivot <=
+// workspace of wp_elems doubles (>= 40 * s * PB).  mode 0: drop iff pivot <=
 // tol (paper); mode 1: SPD (accept iff pivot > 0, flag bit1 otherwise).  The
 // big updates run on `upd` (a second stream) concurrently with the previous
-// one or two panels (lookahead depth by s); ev: 5 events owned by the caller.
+// one or two panels (lookahead depth by s), alternating between the streams
+// upd and upd2 (consecutive updates are independent); ev: 8 events owned by the caller.
 cudaError_t frchol(const double *A, long long lda, int s, double *L, long long ldl, int *piv, int *rk,
                    FactorStats *st, int mode, double *Wp, long long wp_elems, cudaStream_t stream,
-                   cudaStream_t upd, cudaEvent_t *ev);
+                   cudaStream_t upd, cudaStream_t upd2, cudaEvent_t *ev);
+
+// Kernel launches frchol makes for size s (panels + lookahead updates).
+int frchol_launches(int s);
 
 // a5 pieces: Cinv = C^-1 for lower-triangular C (r x r, ldc) padded to
 // r_pad = round_up(r, 32) with an identity block; C and Cinv are r_pad x r_pad
@@ -40,6 +44,8 @@ cudaError_t trtri_lower(double *C, long long ldc, int r, double *Cinv, long long
                         long long part_elems, cudaStream_t stream);
 // Doubles of split-K partial workspace trtri_lower uses for (r, ldc, ldi) (0: no split).
 long long trtri_part_elems(int r, long long ldc, long long ldi);
+// Kernel launches trtri_lower makes with that workspace.
+int trtri_launches(int r, long long ldc, long long ldi, long long part_elems);
 
 // a9: batched small geninv, one CTA per matrix (min(m,n) <= 64, max(m,n) <= 128).  rank[b] >= 0, or
 // -2 (non-finite G) / -3 (L'L not SPD) with G+_b = NaN.  stats (optional, device, one per matrix):

@@ -112,6 +112,18 @@ int trtri_splits(const GemmOp &op) {
   return on ? balanced_splits(op, 8, num_sms()) : 1;
 }
 
+int trtri_launches(int r, long long ldc, long long ldi, long long part_elems) {
+  const int r_pad = (r + 31) / 32 * 32;
+  if (r_pad == 0) return 0;
+  int n = (r_pad > r ? 1 : 0) + 1;
+  for (const GemmOp &op : trtri_ops(nullptr, ldc, r, nullptr, ldi, nullptr)) {
+    int S = trtri_splits(op);
+    while (S > 1 && (long long)S * op.batch * op.M * op.N > part_elems) --S;
+    n += S > 1 ? 2 : 1;
+  }
+  return n;
+}
+
 long long trtri_part_elems(int r, long long ldc, long long ldi) {
   long long need = 0;
   for (const GemmOp &op : trtri_ops(nullptr, ldc, r, nullptr, ldi, nullptr)) {
