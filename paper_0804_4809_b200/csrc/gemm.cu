@@ -1,6 +1,7 @@
 // Host launcher + instantiations of the FP64 DMMA GEMM core (gemm.cuh).
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <array>
@@ -163,8 +164,12 @@ static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
     }
   }
   const double over = 1.0;                              // per-CTA prologue + epilogue, in k-slab units
-  const double red_per_elem = 8.0 / 3.0e12 / 2.1e-6;    // slab units per byte of the reduction (~3 TB/s)
-  const double out_elems = op.lower && !op.mirror ? 0.5 * op.M * (op.M + 1.0) : (double)op.M * op.N;
+  static const double red_bw = [] {                      // bytes/s the reduction streams at (tuning override)
+    const char *v = getenv("GENINV_RED_GBS");
+    return (v ? atof(v) : 3000.0) * 1e9;
+  }();
+  const double red_per_elem = 8.0 / red_bw / 2.1e-6;     // slab units per element of the reduction
+  const double out_elems = op.lower ? 0.5 * op.M * (op.M + 1.0) : (double)op.M * op.N;   // lower: partials lower only
   double best = 1e300;
   int bs = 1;
   for (int S = 1; S <= max_splits; ++S) {
@@ -217,28 +222,35 @@ cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
 // ---------------------------------------------------------------- split-K reduction
 __global__ void splitk_reduce_kernel(const double *__restrict__ P, long long sstride, int splits, long long ldp,
                                      double *__restrict__ out, long long ldo, const double *__restrict__ C0,
-                                     long long ldc0, double alpha, int M, int N, int lower) {
+                                     long long ldc0, double alpha, int M, int N, int lower, int mirror) {
   const long long total = (long long)M * N;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx / N), j = (int)(idx % N);
     if (lower && j > i) continue;
+    double v[16];   // every slice in flight at once (splits <= 16 here; more: the tail loop), summed in order
+#pragma unroll
+    for (int z = 0; z < 16; ++z) v[z] = z < splits ? P[z * sstride + (long long)i * ldp + j] : 0.0;
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += P[z * sstride + (long long)i * ldp + j];
-    double v = alpha * s;
-    if (C0) v += C0[(long long)i * ldc0 + j];
-    out[(long long)i * ldo + j] = v;
+#pragma unroll
+    for (int z = 0; z < 16; ++z)
+      if (z < splits) s += v[z];
+    for (int z = 16; z < splits; ++z) s += P[z * sstride + (long long)i * ldp + j];
+    double o = alpha * s;
+    if (C0) o += C0[(long long)i * ldc0 + j];
+    out[(long long)i * ldo + j] = o;
+    if (mirror && j != i) out[(long long)j * ldo + i] = o;
   }
 }
 
 cudaError_t splitk_reduce(const double *P, long long split_stride, int splits, long long ldp, double *out,
                           long long ldo, const double *C0, long long ldc0, double alpha, int M, int N, bool lower,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool mirror) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   long long total = (long long)M * N;
   int blocks = (int)std::min<long long>((total + 255) / 256, (long long)num_sms() * 16);
   splitk_reduce_kernel<<<blocks, 256, 0, st>>>(P, split_stride, splits, ldp, out, ldo, C0, ldc0, alpha, M, N,
-                                               lower ? 1 : 0);
+                                               lower ? 1 : 0, (lower && mirror) ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -35,9 +35,10 @@ cudaError_t gemm(const GemmOp &op, cudaStream_t st);
 
 // Sum split-K partial slices in a fixed order:  out = C0 + alpha * sum_z P[z]
 // (C0 may be null).  lower: only elements with j <= i (square M == N).
+// (lower && mirror: also out[j][i] = out[i][j], the symmetric store of a lower-only reduction.)
 cudaError_t splitk_reduce(const double *P, long long split_stride, int splits, long long ldp, double *out,
                           long long ldo, const double *C0, long long ldc0, double alpha, int M, int N, bool lower,
-                          cudaStream_t st);
+                          cudaStream_t st, bool mirror = false);
 
 int num_sms();
 

@@ -401,14 +401,15 @@ geninv_status gemm_chain(geninv_handle h, GemmOp op) {
   const double alpha = op.alpha;
   const double *C0 = op.C0;
   const long long ldc0 = op.ldc0;
+  const bool mirror = op.lower && op.mirror;   // partial slices lower only; the reduction stores both halves
   op.C = h->part;
   op.ldc = op.N;
   op.C0 = nullptr;
+  op.mirror = false;
   op.splits = S;
   op.split_stride = pstride;
   GI_TRY(gemm(op, h->st));
-  GI_TRY(splitk_reduce(h->part, pstride, S, op.N, C, ldc, C0, ldc0, alpha, op.M, op.N, op.lower && !op.mirror,
-                       h->st));
+  GI_TRY(splitk_reduce(h->part, pstride, S, op.N, C, ldc, C0, ldc0, alpha, op.M, op.N, op.lower, h->st, mirror));
   h->launches += 2;
   return GENINV_OK;
 }
