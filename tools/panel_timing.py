@@ -5,7 +5,7 @@
 
 Stamps (CTA 0, %globaltimer ns; thread 0 = the diagonal warp, thread 32 = the first row warp):
 0 start, 5 loads done, 1 diagonal-block correction done, 2 diagonal factor done and published
-(thread 0), 4 rows of warp 1 solved, 6 written back (thread 32).
+(thread 0), 7 row correction of warp 1 done, 4 rows of warp 1 solved, 6 written back (thread 32).
 """
 import ctypes
 import os
@@ -33,11 +33,12 @@ np_ = (n + 31) // 32
 buf = (ctypes.c_ulonglong * (np_ * 8))()
 lib.geninv_debug_panel_times(buf, np_)
 t = np.array(buf, dtype=np.float64).reshape(np_, 8)
-d = np.stack([t[:, 5] - t[:, 0], t[:, 1] - t[:, 5], t[:, 2] - t[:, 1], t[:, 4] - t[:, 1], t[:, 6] - t[:, 4],
-              np.maximum(t[:, 2], t[:, 6]) - t[:, 0]], axis=1) / 1e3
+d = np.stack([t[:, 5] - t[:, 0], t[:, 1] - t[:, 5], t[:, 2] - t[:, 1], t[:, 7] - t[:, 1], t[:, 4] - t[:, 1],
+              t[:, 6] - t[:, 4], np.maximum(t[:, 2], t[:, 6]) - t[:, 0]], axis=1) / 1e3
 end = np.maximum(t[:, 2], t[:, 6])
 gap = (t[1:, 0] - end[:-1]) / 1e3
-names = ["loads", "correction", "diag factor", "rows (from correction)", "write-back", "kernel"]
+names = ["loads", "correction", "diag factor", "row correction done", "rows solved (from correction)",
+         "write-back", "kernel"]
 med = np.median(d[2:-1], axis=0)
 print(f"s={n}: {np_} panels; median us per phase (panels >= 2): " +
       ", ".join(f"{a} {b:.2f}" for a, b in zip(names, med)) + f"; gap to next {np.median(gap):.2f}")
