@@ -873,7 +873,20 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
   // ---- output in chunks, D2H of chunk c overlapped with the product of chunk c + 1
   //      N: column block j0..j1 of G+ (n x m) = X G[j0:j1]';  T: row block of G+ = G[:, i0:i1]' X
   // chunk width: a multiple of 16 (even leading dimension of the G+ chunk; 16-aligned TMA strips)
-  const long long cw = std::max<long long>(16, (tr ? target / (m * 8) : target / (ldg * 8)) / 16 * 16);
+  long long cw = std::max<long long>(16, (tr ? target / (m * 8) : target / (ldg * 8)) / 16 * 16);
+  {
+    // round the chunk to whole 128-wide tiles with the best last-wave fill of its (s / 128) x (cw / 128)
+    // output tiles (C3: 1024 -> 1152 columns, 1.73 -> 1.95 waves), within [cw / 2, 2 cw]
+    const long long mt = (s + 127) / 128, sms = num_sms(), nt0 = std::max<long long>(1, cw / 128);
+    double best = -1.0;
+    long long bnt = nt0;
+    for (long long nt = std::max<long long>(1, nt0 / 2); nt <= 2 * nt0; ++nt) {
+      const long long t = mt * nt, waves = (t + sms - 1) / sms;
+      const double fill = (double)t / (double)(waves * sms) - 0.002 * std::llabs(nt - nt0) / nt0;
+      if (fill > best) { best = fill; bnt = nt; }
+    }
+    if (cw >= 128) cw = bnt * 128;
+  }
   const long long total = tr ? n : m;
   const size_t cbytes = (size_t)cw * (s + 1) * sizeof(double) + 256;
   if (cbytes > h->chunk_bytes) {
