@@ -57,7 +57,10 @@ typedef enum {
   GENINV_ENOMEM = 5,      /* device allocation failed */
   GENINV_EALIGN = 6,      /* pointer not 16-byte aligned or odd leading dimension */
   GENINV_ESTATE = 7,      /* geninv_apply_d before geninv_from_gram_d, or shape mismatch */
-  GENINV_ENCCL = 8        /* geninv_sharded_d: libnccl.so.2 not loadable or ncclAllReduce failed */
+  GENINV_ENCCL = 8,       /* geninv_sharded_d: libnccl.so.2 not loadable or ncclAllReduce failed */
+  GENINV_ERANGE = 9       /* an accepted pivot below 2^-1022 (subnormal, ~2.2e-308): |G| is too
+                             small for the branch-free sqrt / reciprocal of the factorisations --
+                             scale G by a power of two (G+ scales by its inverse) */
 } geninv_status;
 
 /* Tolerance policy (SPEC ToleranceConfig).  NULL opts = the paper's policy. */
@@ -104,7 +107,8 @@ GENINV_API geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, i
                        int64_t ldp, int64_t *rank, const geninv_opts *opts, geninv_info *info);
 
 /* Asynchronous variant: nothing is copied back and the stream is not synchronised.  rank_dev
- * (device int64) receives r, or -GENINV_ENONFINITE / -GENINV_ENOTSPD; G+ is then unspecified.
+ * (device int64) receives r, or -GENINV_ENONFINITE / -GENINV_ENOTSPD / -GENINV_ERANGE; G+ is then
+ * unspecified.
  * Without the rank on the host, the inverse runs at the full size s with an identity block past
  * the detected rank (M = diag(M_r, I); K = L M and X = K K' are exactly the rank-r results), so
  * it costs up to (s/r)^3 more inverse flops than geninv_d.  Always the X G' / G' X order. */
@@ -123,7 +127,8 @@ GENINV_API geninv_status geninv_host_d(geninv_handle h, const double *G_host, in
  * `batch` independent m x n matrices: matrix b at G + b*strideG (device, ld >= n),
  * G+ of matrix b written at Gp + b*strideGp (n x m, ldp >= m).  rank_dev:
  * device int32[batch]: the rank of each matrix, or -GENINV_ENONFINITE (-2) /
- * -GENINV_ENOTSPD (-3) for a matrix with non-finite entries / a non-SPD L'L,
+ * -GENINV_ENOTSPD (-3) / -GENINV_ERANGE (-9) for a matrix with non-finite entries / a non-SPD L'L /
+ * an accepted pivot below 2^-1022,
  * whose G+ is then filled with NaN.  Requires min(m, n) <= 64 and
  * max(m, n) <= 128 (GENINV_EINVAL otherwise).  Does not synchronise. */
 GENINV_API geninv_status geninv_batched_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int64_t strideG,

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GENINV_LIB", os.path.join(_HERE, "libgeninv.so"))  # instrumented builds only
 
 GENINV_OK, GENINV_EINVAL, GENINV_ENONFINITE, GENINV_ENOTSPD, GENINV_ECUDA, GENINV_ENOMEM, GENINV_EALIGN, \
-    GENINV_ESTATE, GENINV_ENCCL = range(9)
+    GENINV_ESTATE, GENINV_ENCCL, GENINV_ERANGE = range(10)
 
 
 class GeninvError(RuntimeError):

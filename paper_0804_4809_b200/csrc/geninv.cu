@@ -308,6 +308,7 @@ geninv_status factor(geninv_handle h, const double *A, long long lda, int s, dou
   GI_TRY(cudaStreamSynchronize(h->st));
   *rank_out = r;
   if (hst->flags & 1) return GENINV_ENONFINITE;
+  if (hst->flags & 4) return GENINV_ERANGE;
   return GENINV_OK;
 }
 
@@ -456,7 +457,10 @@ __global__ void identity_tail_kernel(double *B, long long ldb, const int *rk_fin
 }
 __global__ void async_rank_kernel(int64_t *out, const int *rk_final, const FactorStats *fs, const FactorStats *fs2) {
   const int r = *rk_final;
-  *out = (fs->flags & 1) ? -(int64_t)GENINV_ENONFINITE : (r > 0 && (fs2->flags & 2)) ? -(int64_t)GENINV_ENOTSPD : r;
+  *out = (fs->flags & 1)                   ? -(int64_t)GENINV_ENONFINITE
+         : ((fs->flags | fs2->flags) & 4)   ? -(int64_t)GENINV_ERANGE
+         : (r > 0 && (fs2->flags & 2))      ? -(int64_t)GENINV_ENOTSPD
+                                            : r;
 }
 
 // a4-a6 after the factorisation: K = L M (s x r) and, if want_x, X (s x s, full) = K K' = L M M L'.
@@ -614,7 +618,7 @@ geninv_status finish_spd_check(geninv_handle h, int r) {
   int flags = 0;
   GI_TRY(cudaMemcpyAsync(&flags, &h->fs2->flags, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   GI_TRY(cudaStreamSynchronize(h->st));
-  return (flags & 2) ? GENINV_ENOTSPD : GENINV_OK;
+  return (flags & 2) ? GENINV_ENOTSPD : (flags & 4) ? GENINV_ERANGE : GENINV_OK;
 }
 
 bool is_small(long long m, long long n) { return std::min(m, n) <= 64 && std::max(m, n) <= 128; }
@@ -633,7 +637,7 @@ geninv_status small_path(geninv_handle h, const double *G, long long m, long lon
   const int rr = fs->pad;
   h->x_s = -1;
   *r_out = rr < 0 ? 0 : rr;
-  return rr == -2 ? GENINV_ENONFINITE : rr == -3 ? GENINV_ENOTSPD : GENINV_OK;
+  return rr == -2 ? GENINV_ENONFINITE : rr == -3 ? GENINV_ENOTSPD : rr == -9 ? GENINV_ERANGE : GENINV_OK;
 }
 
 }  // namespace
@@ -708,6 +712,7 @@ const char *geninv_strerror(geninv_status st) {
     case GENINV_EALIGN: return "pointer not 16-byte aligned or odd leading dimension";
     case GENINV_ESTATE: return "no factorisation of matching size in the handle";
     case GENINV_ENCCL: return "NCCL unavailable or the all-reduce failed";
+    case GENINV_ERANGE: return "an accepted pivot is subnormal (|G| too small): scale G by a power of two";
   }
   return "unknown status";
 }

@@ -12,7 +12,7 @@ struct FactorStats {
   double max_drop;   // max |dropped pivot|
   double min_pivot;  // min pivot
   double tol;        // tolerance used
-  int flags;         // bit0: non-finite diagonal, bit1: non-SPD pivot (mode 1)
+  int flags;         // bit0: non-finite diagonal, bit1: non-SPD pivot (mode 1), bit2: accepted pivot < 2^-1022
   int pad;           // spare (the one-CTA small path stores the rank here)
 };
 
@@ -48,8 +48,8 @@ long long trtri_part_elems(int r, long long ldc, long long ldi);
 int trtri_launches(int r, long long ldc, long long ldi, long long part_elems);
 
 // a9: batched small geninv, one CTA per matrix (min(m,n) <= 64, max(m,n) <= 128).  rank[b] >= 0, or
-// -2 (non-finite G) / -3 (L'L not SPD) with G+_b = NaN.  stats (optional, device, one per matrix):
-// tol, decision margins and flags (bit0 non-finite, bit1 not SPD) of each matrix.
+// -2 (non-finite G) / -3 (L'L not SPD) / -9 (an accepted pivot below 2^-1022) with G+_b = NaN.  stats (optional, device, one per matrix):
+// tol, decision margins and flags (bit0 non-finite, bit1 not SPD, bit2 pivot < 2^-1022) of each matrix.
 cudaError_t batched_geninv(const double *G, int m, int n, long long ld, long long strideG, long long batch,
                            double *Gp, long long ldp, long long strideGp, int *rank, double tol_rel,
                            double tol_abs, cudaStream_t stream, FactorStats *stats = nullptr);

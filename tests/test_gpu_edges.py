@@ -126,3 +126,37 @@ def test_async_matches_sync(H, m, n, r):
         assert C.rel_fro(Ga.cpu().numpy(), Gs.cpu().numpy()) <= 1e-9
         if R.in_Q():
             assert C.rel_fro(Ga.cpu().numpy(), R.Gp) <= 1e-9
+
+
+@pytest.mark.parametrize("scale", [1e-150, 1e-100, 1e100, 1e150])
+@pytest.mark.parametrize("m,n,r", [(300, 140, 100), (90, 60, 40)])
+def test_extreme_scales(H, scale, m, n, r):
+    """G scaled by 1e+-150 (the Gram's entries near 1e+-300, still normal numbers): the relative
+    tolerance makes the decisions scale-free, so rank and G+ * scale match the unscaled oracle's
+    (the panel kernel's branch-free sqrt / reciprocal assumes normal pivots; the batched path
+    covers the small shape)."""
+    G0 = I.low_rank(31, m, n, r).numpy()
+    R = O.geninv(G0)
+    assert R.in_Q()
+    G = G0 * scale
+    Gp, info = H.geninv_d(dev(G))
+    assert info.rank == R.rank
+    assert C.rel_fro(Gp.cpu().numpy() * scale, R.Gp) <= 1e-9
+
+
+@pytest.mark.parametrize("m,n", [(300, 140), (90, 60)])
+def test_tiny_scale_fails_loudly(H, m, n):
+    """Pivots below 2^-1022 are outside the branch-free sqrt / reciprocal's range: the call reports
+    GENINV_ERANGE (general path) / rank -9 with NaN G+ (batched), never a silent wrong G+."""
+    from paper_0804_4809_b200.binding import GENINV_ERANGE, GeninvError
+    G = I.low_rank(32, m, n, 40).numpy() * 1e-158   # Gram ~1e-313: subnormal pivots
+    with pytest.raises(GeninvError) as exc:
+        H.geninv_d(dev(G))
+    assert exc.value.status == GENINV_ERANGE
+    if max(m, n) > 128:
+        return
+    Gb = torch.as_tensor(G[None]).cuda()
+    Gp, rk = H.geninv_batched_d(Gb)
+    torch.cuda.synchronize()
+    assert int(rk[0]) == -GENINV_ERANGE
+    assert torch.isnan(Gp).all()
