@@ -77,6 +77,7 @@ _SIGS = {
                            ctypes.c_void_p, ctypes.c_void_p],
     "geninv_apply_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                        ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64],
+    "geninv_set_emulation": [ctypes.c_void_p, ctypes.c_int32],
     "geninv_frchol_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
     "geninv_spd_inverse_d": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
@@ -143,6 +144,10 @@ class Handle:
         self._h = h
         self._lib = lib
         self.use_stream(torch.cuda.current_stream(self.device))
+
+    def set_emulation(self, mode: int):
+        """a7 arithmetic: 0 = FP64 tensor cores (DMMA, default), 1 = emulated on the INT8 tensor cores."""
+        _check(self._lib.geninv_set_emulation(self._h, int(mode)))
 
     def use_stream(self, stream: torch.cuda.Stream):
         _check(self._lib.geninv_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)))

@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "../../include/geninv.h"
+#include "emu.h"
 #include "gemm_host.h"
 #include "kernels.h"
 
@@ -52,6 +53,12 @@ struct geninv_handle_s {
   // least-squares solve (f1): the s x k intermediate G'F or X F
   double *T1 = nullptr;
   size_t t1_bytes = 0;
+  // a7 emulated on the INT8 tensor cores (geninv_set_emulation): slices of X and of a chunk of G
+  int emulate = -1;        // -1: not set (GENINV_EMULATE decides), 0 native DMMA, 1 emulated
+  int8_t *emu_x = nullptr, *emu_g = nullptr;
+  int *emu_ex = nullptr, *emu_eg = nullptr, *emu_flag = nullptr;
+  double *emu_sc = nullptr;
+  size_t emu_x_bytes = 0, emu_g_bytes = 0, emu_ex_n = 0, emu_eg_n = 0, emu_sc_n = 0;
   // state of the last factorisation (for geninv_apply_d)
   int x_s = -1;
   int last_rank = 0;
@@ -538,9 +545,69 @@ geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n
 }
 
 // a7: Gp = X G' (trans 0: Gp is n x m) or G' X (trans 1: Gp is n x m).
+bool emulation_on(geninv_handle h) {
+  if (h->emulate >= 0) return h->emulate != 0;
+  static const int env = [] {
+    const char *e = getenv("GENINV_EMULATE");
+    return e ? atoi(e) : 0;
+  }();
+  return env != 0;
+}
+
+template <typename T>
+geninv_status grow(T *&p, size_t &have, size_t need) {
+  if (need <= have) return GENINV_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  have = 0;
+  GI_TRY(cudaMalloc(&p, need * sizeof(T)));
+  have = need;
+  return GENINV_OK;
+}
+
+// a7 (N branch) on the INT8 tensor cores: Gp (s x m) = X G' from S = 8 int8 slices of X and of
+// row chunks of G (Ozaki splitting, emu.cu).  Returns GENINV_ERANGE (nothing usable written) if a
+// row of X or G is outside the exact power-of-two scaling range; the caller then uses DMMA.
+geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
+                             long long ldp, cudaStream_t st) {
+  static const int T = [] {
+    const char *e = getenv("GENINV_EMU_T");
+    const int t = e ? atoi(e) : 9;
+    return t >= 2 && t <= 16 ? t : 9;
+  }();
+  constexpr int S = 8;
+  const int s = (int)n, Kp = emu_kpad(s);
+  const long long chunk = std::max<long long>(256, std::min<long long>(m, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
+  GI_TRYS(grow(h->emu_x, h->emu_x_bytes, (size_t)S * s * Kp));
+  GI_TRYS(grow(h->emu_ex, h->emu_ex_n, (size_t)s));
+  GI_TRYS(grow(h->emu_g, h->emu_g_bytes, (size_t)S * std::min<long long>(chunk, m) * Kp));
+  GI_TRYS(grow(h->emu_eg, h->emu_eg_n, (size_t)std::min<long long>(chunk, m)));
+  GI_TRYS(grow(h->emu_sc, h->emu_sc_n, (size_t)emu_scratch_elems(s, (int)std::min<long long>(chunk, m))));
+  if (!h->emu_flag) {
+    GI_TRY(cudaMalloc(&h->emu_flag, sizeof(int)));
+  }
+  GI_TRY(cudaMemsetAsync(h->emu_flag, 0, sizeof(int), st));
+  GI_TRY(emu_split(h->X, h->ld, s, s, S, h->emu_x, h->emu_ex, h->emu_flag, st));
+  h->launches += 1;
+  for (long long j0 = 0; j0 < m; j0 += chunk) {
+    const int nc = (int)std::min<long long>(chunk, m - j0);
+    GI_TRY(emu_split(G + j0 * ld, ld, nc, s, S, h->emu_g, h->emu_eg, h->emu_flag, st));
+    GI_TRY(emu_gemm_nt(h->emu_x, h->emu_ex, s, h->emu_g, h->emu_eg, nc, s, S, T, Gp + j0, ldp, h->emu_sc, st));
+    h->launches += 2;
+  }
+  int flag = 0;
+  GI_TRY(cudaMemcpyAsync(&flag, h->emu_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GI_TRY(cudaStreamSynchronize(st));
+  return flag ? GENINV_ERANGE : GENINV_OK;
+}
+
 geninv_status apply(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *Gp,
                     long long ldp, cudaStream_t st) {
   const long long s = trans ? m : n;
+  if (!trans && emulation_on(h) && s <= 16384) {
+    const geninv_status es = apply_emulated(h, G, m, n, ld, Gp, ldp, st);
+    if (es != GENINV_ERANGE) return es;   // out of the emulation's range: the native product below
+  }
   GemmOp op;
   if (!trans) {
     // Gp[i][j] = sum_k X[i][k] G[j][k],  i < n = s, j < m
@@ -673,6 +740,12 @@ geninv_status geninv_set_stream(geninv_handle h, void *stream) {
   return GENINV_OK;
 }
 
+geninv_status geninv_set_emulation(geninv_handle h, int mode) {
+  if (!h || mode < 0 || mode > 1) return GENINV_EINVAL;
+  h->emulate = mode;
+  return GENINV_OK;
+}
+
 geninv_status geninv_destroy(geninv_handle h) {
   if (!h) return GENINV_EINVAL;
   cudaSetDevice(h->device);
@@ -681,6 +754,9 @@ geninv_status geninv_destroy(geninv_handle h) {
   if (h->part) cudaFree(h->part);
   if (h->Gdev) cudaFree(h->Gdev);
   if (h->T1) cudaFree(h->T1);
+  for (void *p : {(void *)h->emu_x, (void *)h->emu_g, (void *)h->emu_ex, (void *)h->emu_eg, (void *)h->emu_flag,
+                  (void *)h->emu_sc})
+    if (p) cudaFree(p);
   for (auto &c : h->Gpchunk)
     if (c) cudaFree(c);
   for (auto &ev : h->ev)
