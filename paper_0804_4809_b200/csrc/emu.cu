@@ -59,6 +59,9 @@ GI_DEV void mma_commit(uint64_t *bar) {
 }
 GI_DEV double pow2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }   // 2^e, |e| <= 1022
 
+// Persistent: CTA c takes tiles c, c + gridDim.x, ... (tile = m-tile fastest, so CTAs working at the
+// same time share the B slices of one n-tile); the stage ring, the TMEM ping-pong and the scratch tile
+// carry over from one tile to the next, so a tile's last epilogue overlaps the next tile's MMAs.
 __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                           const __grid_constant__ CUtensorMap tmB,
                                                           const int *__restrict__ ea, const int *__restrict__ eb,
@@ -73,8 +76,8 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
   uint32_t *tslot = (uint32_t *)(accempty + 2);
   int *s_eb = (int *)(smem + ESTAGES * ESTAGE_BYTES + 512);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m0 = blockIdx.x * EBM, n0 = blockIdx.y * EBN;
   const int nk = (Kp + EBK - 1) / EBK;
+  const int mt = (M + EBM - 1) / EBM, ntiles = mt * ((N + EBN - 1) / EBN);
   if (tid == 0) {
     for (int i = 0; i < ESTAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -86,7 +89,6 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
     }
     fence_barrier_init();
   }
-  for (int j = tid; j < EBN; j += ENT) s_eb[j] = n0 + j < N ? eb[n0 + j] : 0;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                  "r"(512));
@@ -98,103 +100,114 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
-    if (lane == 0) {   // TMA producer over (group, pair, k-slab)
+    if (lane == 0) {   // TMA producer over (tile, group, pair, k-slab)
       tma_prefetch(&tmA);
       tma_prefetch(&tmB);
       int it = 0;
-      for (int g = T; g >= 2; --g)
-        for (int t = max(1, g - S); t <= min(S, g - 1); ++t)
-          for (int kb = 0; kb < nk; ++kb, ++it) {
-            const int st = it % ESTAGES;
-            if (it >= ESTAGES) mbar_wait(&empty[st], ((it / ESTAGES) & 1) ^ 1);
-            uint8_t *sA = smem + st * ESTAGE_BYTES, *sB = sA + EA_BYTES;
-            mbar_arrive_expect_tx(&full[st], ESTAGE_BYTES);
-            tma_load_3d_u8(sA, &tmA, &full[st], kb * EBK, m0, t - 1);
-            tma_load_3d_u8(sB, &tmB, &full[st], kb * EBK, n0, g - t - 1);
-          }
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (tile % mt) * EBM, n0 = (tile / mt) * EBN;
+        for (int g = T; g >= 2; --g)
+          for (int t = max(1, g - S); t <= min(S, g - 1); ++t)
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+              const int st = it % ESTAGES;
+              if (it >= ESTAGES) mbar_wait(&empty[st], ((it / ESTAGES) & 1) ^ 1);
+              uint8_t *sA = smem + st * ESTAGE_BYTES, *sB = sA + EA_BYTES;
+              mbar_arrive_expect_tx(&full[st], ESTAGE_BYTES);
+              tma_load_3d_u8(sA, &tmA, &full[st], kb * EBK, m0, t - 1);
+              tma_load_3d_u8(sB, &tmB, &full[st], kb * EBK, n0, g - t - 1);
+            }
+      }
     }
   } else if (warp == 1) {
-    if (lane == 0) {   // MMA issuer: group q into TMEM buffer q & 1
+    if (lane == 0) {   // MMA issuer: the q-th group (over all tiles) into TMEM buffer q & 1
       int it = 0, q = 0;
-      for (int g = T; g >= 2; --g, ++q) {
-        const int buf = q & 1;
-        if (q >= 2) mbar_wait(&accempty[buf], ((q >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem + buf * EBN;
-        uint32_t accumulate = 0;
-        for (int t = max(1, g - S); t <= min(S, g - 1); ++t)
-          for (int kb = 0; kb < nk; ++kb, ++it) {
-            const int st = it % ESTAGES;
-            mbar_wait(&full[st], (it / ESTAGES) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t a0 = smem_u32(smem + st * ESTAGE_BYTES), b0 = a0 + EA_BYTES;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int g = T; g >= 2; --g, ++q) {
+          const int buf = q & 1;
+          if (q >= 2) mbar_wait(&accempty[buf], ((q >> 1) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t acc = tmem + buf * EBN;
+          uint32_t accumulate = 0;
+          for (int t = max(1, g - S); t <= min(S, g - 1); ++t)
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+              const int st = it % ESTAGES;
+              mbar_wait(&full[st], (it / ESTAGES) & 1);
+              asm volatile("tcgen05.fence::after_thread_sync;");
+              const uint32_t a0 = smem_u32(smem + st * ESTAGE_BYTES), b0 = a0 + EA_BYTES;
 #pragma unroll
-            for (int kk = 0; kk < EBK / 32; ++kk) {
-              mma_i8(acc, umma_desc(a0 + 32 * kk), umma_desc(b0 + 32 * kk), accumulate);
-              accumulate = 1;
+              for (int kk = 0; kk < EBK / 32; ++kk) {
+                mma_i8(acc, umma_desc(a0 + 32 * kk), umma_desc(b0 + 32 * kk), accumulate);
+                accumulate = 1;
+              }
+              mma_commit(&empty[st]);   // the stage is free once these MMAs have read it
             }
-            mma_commit(&empty[st]);   // the stage is free once these MMAs have read it
-          }
-        mma_commit(&accfull[buf]);
-      }
+          mma_commit(&accfull[buf]);
+        }
     }
   } else {
-    // epilogue warps 2..5: TMEM lane quarter warp & 3 = rows m0 + 32 (warp & 3) + lane
+    // epilogue warps 2..5: TMEM lane quarter warp & 3 = tile rows 32 (warp & 3) + lane.  The running sum
+    // lives in this CTA's scratch tile, column-major ([c][row]: a warp's 32 rows are 256 contiguous
+    // bytes, every access coalesced); the last group (g = 2) adds it into C.
     const int quarter = warp & 3;
-    const int row = m0 + 32 * quarter + lane;
-    const int ea_r = row < M ? ea[row] : 0;
-    double *crow = C + (long long)row * ldc;
+    double *sc0 = scratch + (long long)blockIdx.x * EBN * EBM + 32 * quarter + lane;
     int q = 0;
-    for (int g = T; g >= 2; --g, ++q) {
-      const int buf = q & 1;
-      mbar_wait(&accfull[buf], (q >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const double sr = pow2i(ea_r - 7 * g);
-      for (int c0 = 0; c0 < EBN; c0 += 32) {
-        uint32_t r[32];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-              "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-              "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-              "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-            : "r"(tmem + buf * EBN + ((uint32_t)(32 * quarter) << 16) + c0));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-        // running sum in the CTA's scratch tile, column-major ([c][row]: a warp's 32 rows are 256
-        // contiguous bytes, every access coalesced and page-local); the last group adds it into C
-        const bool last = g == 2;
-        double *sc = scratch + ((long long)(blockIdx.y * gridDim.x + blockIdx.x) * EBN + c0) * EBM + 32 * quarter + lane;
-        double o[32];
-        if (q > 0) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int m0 = (tile % mt) * EBM, n0 = (tile / mt) * EBN;
+      const int row = m0 + 32 * quarter + lane;
+      const int ea_r = row < M ? ea[row] : 0;
+      double *crow = C + (long long)row * ldc;
+      asm volatile("bar.sync 1, 128;" ::: "memory");   // the previous tile's s_eb is no longer read
+      for (int j = tid - 64; j < EBN; j += 128) s_eb[j] = n0 + j < N ? eb[n0 + j] : 0;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int g = T; g >= 2; --g, ++q) {
+        const int buf = q & 1;
+        const bool first = g == T, last = g == 2;
+        mbar_wait(&accfull[buf], (q >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const double sr = pow2i(ea_r - 7 * g);
+        for (int c0 = 0; c0 < EBN; c0 += 32) {
+          uint32_t r[32];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(tmem + buf * EBN + ((uint32_t)(32 * quarter) << 16) + c0));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          double *sc = sc0 + (long long)c0 * EBM;
+          double o[32];
+          if (!first) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __ldcg(sc + j * EBM);
-        }
+            for (int j = 0; j < 32; ++j) o[j] = __ldcg(sc + j * EBM);
+          }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double v = (double)(int)r[j] * sr * pow2i(s_eb[c0 + j]);
-          o[j] = q > 0 ? o[j] + v : v;
-        }
-        if (!last) {
+          for (int j = 0; j < 32; ++j) {
+            const double v = (double)(int)r[j] * sr * pow2i(s_eb[c0 + j]);
+            o[j] = first ? v : o[j] + v;
+          }
+          if (!last) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) __stcg(sc + j * EBM, o[j]);
-        } else if (row < M) {
-          const int nb = n0 + c0;
-          if (nb + 32 <= N && !(ldc & 1)) {
-            double2 *d2 = reinterpret_cast<double2 *>(crow + nb);
+            for (int j = 0; j < 32; ++j) __stcg(sc + j * EBM, o[j]);
+          } else if (row < M) {
+            const int nb = n0 + c0;
+            if (nb + 32 <= N && !(ldc & 1)) {
+              double2 *d2 = reinterpret_cast<double2 *>(crow + nb);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) d2[j] = make_double2(o[2 * j], o[2 * j + 1]);
-          } else {
+              for (int j = 0; j < 16; ++j) d2[j] = make_double2(o[2 * j], o[2 * j + 1]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (nb + j < N) crow[nb + j] = o[j];
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < N) crow[nb + j] = o[j];
+            }
           }
         }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&accempty[buf]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&accempty[buf]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -276,6 +289,17 @@ cudaError_t slice_map(CUtensorMap *m, const int8_t *p, int rows, int Kp, int S, 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+int num_sms_emu() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
 }  // namespace
 
 int emu_kpad(int K) { return (K + 15) / 16 * 16; }
@@ -289,9 +313,12 @@ cudaError_t emu_split(const double *X, long long ldx, int rows, int K, int S, in
   return cudaGetLastError();
 }
 
-long long emu_scratch_elems(int M, int N) {
-  return (long long)((M + EBM - 1) / EBM) * ((N + EBN - 1) / EBN) * EBM * EBN;
+static int emu_ctas(int M, int N) {
+  const long long tiles = (long long)((M + EBM - 1) / EBM) * ((N + EBN - 1) / EBN);
+  return (int)std::min<long long>(tiles, num_sms_emu());
 }
+
+long long emu_scratch_elems(int M, int N) { return (long long)emu_ctas(M, N) * EBM * EBN; }
 
 cudaError_t emu_gemm_nt(const int8_t *As, const int *ea, int M, const int8_t *Bs, const int *eb, int N, int K, int S,
                         int T, double *C, long long ldc, double *scratch, cudaStream_t st) {
@@ -307,8 +334,7 @@ cudaError_t emu_gemm_nt(const int8_t *As, const int *ea, int M, const int8_t *Bs
       return e;
     attr = true;
   }
-  dim3 grid((M + EBM - 1) / EBM, (N + EBN - 1) / EBN);
-  emu_gemm_kernel<<<grid, ENT, ESMEM, st>>>(ta, tb, ea, eb, C, ldc, M, N, Kp, S, T, scratch);
+  emu_gemm_kernel<<<emu_ctas(M, N), ENT, ESMEM, st>>>(ta, tb, ea, eb, C, ldc, M, N, Kp, S, T, scratch);
   return cudaGetLastError();
 }
 
