@@ -57,7 +57,30 @@ GI_DEV void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+#define GI_DEV_HOST_INLINE __host__ __device__ __forceinline__
 GI_DEV double pow2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }   // 2^e, |e| <= 1022
+
+// Tiles of a square output's lower triangle (128 x 256 tiles: column block nj holds row blocks
+// 2 nj .. mt - 1; the upper halves inside them are computed too, never read).
+GI_DEV_HOST_INLINE int lower_tiles(int mt, int ntn) {
+  int n = 0;
+  for (int nj = 0; nj < ntn; ++nj) n += mt - 2 * nj > 0 ? mt - 2 * nj : 0;
+  return n;
+}
+GI_DEV void tile_origin(int tile, int mt, int lower, int &m0, int &n0) {
+  if (!lower) {
+    m0 = (tile % mt) * EBM;
+    n0 = (tile / mt) * EBN;
+    return;
+  }
+  int nj = 0;
+  while (tile >= mt - 2 * nj) {
+    tile -= mt - 2 * nj;
+    ++nj;
+  }
+  m0 = (2 * nj + tile) * EBM;
+  n0 = nj * EBN;
+}
 
 // Persistent: CTA c takes tiles c, c + gridDim.x, ... (tile = m-tile fastest, so CTAs working at the
 // same time share the B slices of one n-tile); the stage ring, the TMEM ping-pong and the scratch tile
@@ -66,7 +89,8 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
                                                           const __grid_constant__ CUtensorMap tmB,
                                                           const int *__restrict__ ea, const int *__restrict__ eb,
                                                           double *__restrict__ C, long long ldc, int M, int N,
-                                                          int Kp, int S, int T, double *__restrict__ scratch) {
+                                                          int Kp, int S, int T, double *__restrict__ scratch,
+                                                          int lower, int accumulate) {
   extern __shared__ uint8_t emu_smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)emu_smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t *full = (uint64_t *)(smem + ESTAGES * ESTAGE_BYTES);
@@ -77,7 +101,8 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
   int *s_eb = (int *)(smem + ESTAGES * ESTAGE_BYTES + 512);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nk = (Kp + EBK - 1) / EBK;
-  const int mt = (M + EBM - 1) / EBM, ntiles = mt * ((N + EBN - 1) / EBN);
+  const int mt = (M + EBM - 1) / EBM, ntn = (N + EBN - 1) / EBN;
+  const int ntiles = lower ? lower_tiles(mt, ntn) : mt * ntn;
   if (tid == 0) {
     for (int i = 0; i < ESTAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -105,7 +130,8 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
       tma_prefetch(&tmB);
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (tile % mt) * EBM, n0 = (tile / mt) * EBN;
+        int m0, n0;
+        tile_origin(tile, mt, lower, m0, n0);
         for (int g = T; g >= 2; --g)
           for (int t = max(1, g - S); t <= min(S, g - 1); ++t)
             for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -152,7 +178,8 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
     double *sc0 = scratch + (long long)blockIdx.x * EBN * EBM + 32 * quarter + lane;
     int q = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int m0 = (tile % mt) * EBM, n0 = (tile / mt) * EBN;
+      int m0, n0;
+      tile_origin(tile, mt, lower, m0, n0);
       const int row = m0 + 32 * quarter + lane;
       const int ea_r = row < M ? ea[row] : 0;
       double *crow = C + (long long)row * ldc;
@@ -195,12 +222,20 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
             const int nb = n0 + c0;
             if (nb + 32 <= N && !(ldc & 1)) {
               double2 *d2 = reinterpret_cast<double2 *>(crow + nb);
+              if (accumulate) {   // C += this pass (the Gram over K-chunks), old values loaded first
+                double2 c[16];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) d2[j] = make_double2(o[2 * j], o[2 * j + 1]);
+                for (int j = 0; j < 16; ++j) c[j] = d2[j];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) d2[j] = make_double2(c[j].x + o[2 * j], c[j].y + o[2 * j + 1]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) d2[j] = make_double2(o[2 * j], o[2 * j + 1]);
+              }
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (nb + j < N) crow[nb + j] = o[j];
+                if (nb + j < N) crow[nb + j] = accumulate ? crow[nb + j] + o[j] : o[j];
             }
           }
         }
@@ -261,6 +296,79 @@ __global__ void emu_split_kernel(const double *__restrict__ X, long long ldx, in
   }
 }
 
+// Column maxima of |G| over rows [0, rows) of a row-major block (the N-branch Gram's K-chunk):
+// bit patterns of non-negative doubles order like the doubles, so atomicMax on them is exact.
+__global__ void emu_colmax_kernel(const double *__restrict__ G, long long ld, int rows, int cols,
+                                  unsigned long long *__restrict__ mx) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int r0 = blockIdx.y * 256, r1 = min(rows, r0 + 256);
+  double m = 0.0;
+  for (int r = r0; r < r1; ++r) m = fmax(m, fabs(G[(long long)r * ld + c]));
+  atomicMax(mx + c, (unsigned long long)__double_as_longlong(m));
+}
+
+GI_DEV int emu_exponent(double mx, int *flag) {
+  int e = 0;
+  if (mx > 0.0) {
+    frexp(mx * (128.0 / 127.0), &e);
+    if (!(mx * (128.0 / 127.0) < ldexp(1.0, e))) ++e;
+  }
+  if (!isfinite(mx) || e < -900 || e > 900) {
+    atomicOr(flag, 1);
+    e = 0;
+  }
+  return e;
+}
+
+// Digits of the COLUMNS of a row-major block (rows x cols): planes [S][cols][Kp] with Kp = padded rows,
+// i.e. the K-major operand of G'G for this K-chunk.  Block: 128 rows x 32 columns through shared
+// memory; warp w writes columns w, w + 8, .. as 128 contiguous bytes per plane.
+__global__ void __launch_bounds__(256) emu_split_cols_kernel(const double *__restrict__ G, long long ld, int rows,
+                                                            int cols, int Kp, int S,
+                                                            const unsigned long long *__restrict__ mx,
+                                                            int8_t *__restrict__ sl, int *__restrict__ ex,
+                                                            int *flag) {
+  __shared__ double t[32][129];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 128;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = warp; i < 128; i += 8) {
+    const int r = r0 + i, c = c0 + lane;
+    t[lane][i] = (r < rows && c < cols) ? G[(long long)r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  const long long plane = (long long)cols * Kp;
+  for (int cc = warp; cc < 32; cc += 8) {
+    const int c = c0 + cc;
+    if (c >= cols) break;
+    const int e = emu_exponent(__longlong_as_double((long long)mx[c]), flag);
+    if (blockIdx.y == 0 && lane == 0) ex[c] = e;
+    const double inv = ldexp(1.0, -e);
+    const int k = r0 + 4 * lane;
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = t[cc][4 * lane + q] * inv;
+    int8_t *out = sl + (long long)c * Kp;
+    for (int tt = 0; tt < S; ++tt) {
+      signed char d[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double y = v[q] * 128.0;
+        const double rr = rint(y);
+        d[q] = (signed char)(int)rr;
+        v[q] = y - rr;
+      }
+      if (k + 3 < Kp) {
+        char4 c4;
+        c4.x = d[0]; c4.y = d[1]; c4.z = d[2]; c4.w = d[3];
+        *reinterpret_cast<char4 *>(out + tt * plane + k) = c4;
+      } else {
+        for (int q = 0; q < 4 && k + q < Kp; ++q) out[tt * plane + k + q] = d[q];
+      }
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_enc8 = nullptr;
 
 cudaError_t get_enc8() {
@@ -313,15 +421,17 @@ cudaError_t emu_split(const double *X, long long ldx, int rows, int K, int S, in
   return cudaGetLastError();
 }
 
-static int emu_ctas(int M, int N) {
-  const long long tiles = (long long)((M + EBM - 1) / EBM) * ((N + EBN - 1) / EBN);
+static int emu_ctas(int M, int N, int lower) {
+  const int mt = (M + EBM - 1) / EBM, ntn = (N + EBN - 1) / EBN;
+  const long long tiles = lower ? lower_tiles(mt, ntn) : (long long)mt * ntn;
   return (int)std::min<long long>(tiles, num_sms_emu());
 }
 
-long long emu_scratch_elems(int M, int N) { return (long long)emu_ctas(M, N) * EBM * EBN; }
+long long emu_scratch_elems(int M, int N) { return (long long)emu_ctas(M, N, 0) * EBM * EBN; }
 
 cudaError_t emu_gemm_nt(const int8_t *As, const int *ea, int M, const int8_t *Bs, const int *eb, int N, int K, int S,
-                        int T, double *C, long long ldc, double *scratch, cudaStream_t st) {
+                        int T, double *C, long long ldc, double *scratch, cudaStream_t st, int lower,
+                        int accumulate) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   const int Kp = emu_kpad(K);
   CUtensorMap ta, tb;
@@ -334,7 +444,21 @@ cudaError_t emu_gemm_nt(const int8_t *As, const int *ea, int M, const int8_t *Bs
       return e;
     attr = true;
   }
-  emu_gemm_kernel<<<emu_ctas(M, N), ENT, ESMEM, st>>>(ta, tb, ea, eb, C, ldc, M, N, Kp, S, T, scratch);
+  emu_gemm_kernel<<<emu_ctas(M, N, lower), ENT, ESMEM, st>>>(ta, tb, ea, eb, C, ldc, M, N, Kp, S, T, scratch,
+                                                              lower, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t emu_split_cols(const double *G, long long ld, int rows, int cols, int S, int8_t *slices, int *exps,
+                           unsigned long long *colmax, int *flag, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const int Kp = emu_kpad(rows);
+  cudaError_t e = cudaMemsetAsync(colmax, 0, (size_t)cols * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  emu_colmax_kernel<<<dim3((cols + 127) / 128, (rows + 255) / 256), 128, 0, st>>>(G, ld, rows, cols, colmax);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  emu_split_cols_kernel<<<dim3((cols + 31) / 32, (Kp + 127) / 128), 256, 0, st>>>(G, ld, rows, cols, Kp, S, colmax,
+                                                                                 slices, exps, flag);
   return cudaGetLastError();
 }
 

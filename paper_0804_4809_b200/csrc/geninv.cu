@@ -58,7 +58,8 @@ struct geninv_handle_s {
   int8_t *emu_x = nullptr, *emu_g = nullptr;
   int *emu_ex = nullptr, *emu_eg = nullptr, *emu_flag = nullptr;
   double *emu_sc = nullptr;
-  size_t emu_x_bytes = 0, emu_g_bytes = 0, emu_ex_n = 0, emu_eg_n = 0, emu_sc_n = 0;
+  unsigned long long *emu_cm = nullptr;
+  size_t emu_x_bytes = 0, emu_g_bytes = 0, emu_ex_n = 0, emu_eg_n = 0, emu_sc_n = 0, emu_cm_n = 0;
   // state of the last factorisation (for geninv_apply_d)
   int x_s = -1;
   int last_rank = 0;
@@ -162,10 +163,67 @@ int pick_splits(long long tiles, long long nslab) {
   return 1;
 }
 
+bool emulation_on(geninv_handle h) {
+  if (h->emulate >= 0) return h->emulate != 0;
+  static const int env = [] {
+    const char *e = getenv("GENINV_EMULATE");
+    return e ? atoi(e) : 0;
+  }();
+  return env != 0;
+}
+
+template <typename T>
+geninv_status grow(T *&p, size_t &have, size_t need) {
+  if (need <= have) return GENINV_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  have = 0;
+  GI_TRY(cudaMalloc(&p, need * sizeof(T)));
+  have = need;
+  return GENINV_OK;
+}
+
+// a1 on the INT8 tensor cores (geninv_set_emulation): K-chunks of <= 16384 lines of G (the int32
+// group sums stay exact), each split into 8 int8 digits per column (N) / row (T) of the chunk, the
+// lower tiles of A accumulated chunk after chunk in FP64 (fixed order: deterministic).  GENINV_ERANGE:
+// a line outside the exact-scaling range (the caller then runs the DMMA Gram).
+geninv_status gram_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans,
+                            double *A, long long lda, bool accumulate) {
+  constexpr int S = 8, T = 9, KC = 16384;
+  const long long s = trans ? m : n, ell = trans ? n : m;
+  const int Kp = emu_kpad(KC);
+  GI_TRYS(grow(h->emu_g, h->emu_g_bytes, (size_t)S * s * Kp));
+  GI_TRYS(grow(h->emu_eg, h->emu_eg_n, (size_t)s));
+  GI_TRYS(grow(h->emu_cm, h->emu_cm_n, (size_t)s));
+  GI_TRYS(grow(h->emu_sc, h->emu_sc_n, (size_t)emu_scratch_elems((int)s, (int)s)));
+  if (!h->emu_flag) GI_TRY(cudaMalloc(&h->emu_flag, sizeof(int)));
+  GI_TRY(cudaMemsetAsync(h->emu_flag, 0, sizeof(int), h->st));
+  for (long long k0 = 0; k0 < ell; k0 += KC) {
+    const int kc = (int)std::min<long long>(KC, ell - k0);
+    if (!trans)
+      GI_TRY(emu_split_cols(G + k0 * ld, ld, kc, (int)s, S, h->emu_g, h->emu_eg, h->emu_cm, h->emu_flag, h->st));
+    else
+      GI_TRY(emu_split(G + k0, ld, (int)s, kc, S, h->emu_g, h->emu_eg, h->emu_flag, h->st));
+    GI_TRY(emu_gemm_nt(h->emu_g, h->emu_eg, (int)s, h->emu_g, h->emu_eg, (int)s, kc, S, T, A, lda, h->emu_sc, h->st,
+                       1, (k0 > 0 || accumulate) ? 1 : 0));
+    h->launches += trans ? 2 : 3;
+  }
+  int flag = 0;
+  GI_TRY(cudaMemcpyAsync(&flag, h->emu_flag, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  GI_TRY(cudaStreamSynchronize(h->st));
+  return flag ? GENINV_ERANGE : GENINV_OK;
+}
+
 // a1: A (s x s, lower) = G'G (trans == 0) or GG' (trans == 1).
 geninv_status gram(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *A,
                    long long lda, const double *accumulate = nullptr) {
   const long long s = trans ? m : n, ell = trans ? n : m;
+  // emulated Gram: only where its 128 x 256 lower tiles fill the machine (s >= 3072: >= 170 tiles);
+  // an accumulating call could not fall back after a range flag
+  if (emulation_on(h) && !accumulate && s >= 3072 && s <= 16384) {
+    const geninv_status es = gram_emulated(h, G, m, n, ld, trans, A, lda, false);
+    if (es != GENINV_ERANGE) return es;   // out of the emulation's range: the DMMA Gram below
+  }
   GemmOp op;
   op.A = Mat{G, ld, m, n};
   op.B = op.A;
@@ -545,26 +603,6 @@ geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n
 }
 
 // a7: Gp = X G' (trans 0: Gp is n x m) or G' X (trans 1: Gp is n x m).
-bool emulation_on(geninv_handle h) {
-  if (h->emulate >= 0) return h->emulate != 0;
-  static const int env = [] {
-    const char *e = getenv("GENINV_EMULATE");
-    return e ? atoi(e) : 0;
-  }();
-  return env != 0;
-}
-
-template <typename T>
-geninv_status grow(T *&p, size_t &have, size_t need) {
-  if (need <= have) return GENINV_OK;
-  if (p) cudaFree(p);
-  p = nullptr;
-  have = 0;
-  GI_TRY(cudaMalloc(&p, need * sizeof(T)));
-  have = need;
-  return GENINV_OK;
-}
-
 // a7 (N branch) on the INT8 tensor cores: Gp (s x m) = X G' from S = 8 int8 slices of X and of
 // row chunks of G (Ozaki splitting, emu.cu).  Returns GENINV_ERANGE (nothing usable written) if a
 // row of X or G is outside the exact power-of-two scaling range; the caller then uses DMMA.
@@ -755,7 +793,7 @@ geninv_status geninv_destroy(geninv_handle h) {
   if (h->Gdev) cudaFree(h->Gdev);
   if (h->T1) cudaFree(h->T1);
   for (void *p : {(void *)h->emu_x, (void *)h->emu_g, (void *)h->emu_ex, (void *)h->emu_eg, (void *)h->emu_flag,
-                  (void *)h->emu_sc})
+                  (void *)h->emu_sc, (void *)h->emu_cm})
     if (p) cudaFree(p);
   for (auto &c : h->Gpchunk)
     if (c) cudaFree(c);

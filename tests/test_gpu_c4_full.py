@@ -6,7 +6,8 @@ G'G (the listing's `G'*G`), then its own tolerance / full-rank Cholesky /
 chain (oracle.from_gram).  Compared: the detected rank and pivot list (exact, inputs in Q),
 X = L M M L' (relative), and sampled columns of G+ = X G' (relative); plus full-size Penrose
 conditions on the GPU with cuBLAS (torch.matmul, a test-only checker independent of the library).
-Needs ~130 GiB of HBM and ~70 GiB of host RAM; takes a few minutes.
+Needs ~130 GiB of HBM and ~70 GiB of host RAM; takes a few minutes.  Run for the native path and
+for the INT8-emulated Gram and a7.
 """
 import os
 
@@ -21,13 +22,16 @@ from paper_0804_4809_b200 import inputs as I
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def test_c4_full_size():
+@pytest.mark.parametrize("emulate", [0, 1], ids=["dmma", "int8_emulated"])
+def test_c4_full_size(emulate):
+    """emulate = 1: the Gram and a7 on the INT8 tensor cores (geninv_set_emulation)."""
     from paper_0804_4809_b200.binding import Handle
     from paper_0804_4809_b200.sharded import CudaBackend, sharded_geninv
 
     cfg = I.CONFIGS["C4"]
     m, n = cfg.m, cfg.n
     h = Handle(0)
+    h.set_emulation(emulate)
     be = CudaBackend(h)
     seed = int(os.environ.get("GENINV_C4_SEED", I.QSEED["C4"]))   # override: screening candidate seeds
     G = I.make_single(cfg, seed, device="cuda")
