@@ -478,7 +478,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if not args.emulate else
-            "f64 (a7 emulated: 8 int8 digits per element, 36 exact int32 digit products, FP64 accumulation)",
+            ("f64 (Gram and a7 emulated on INT8 tensor cores: 8 int8 digits per element, 36 exact int32 digit "
+             "products, FP64 accumulation)" if not tr else "f64 (Gram emulated on INT8 tensor cores; a7 on DMMA)"),
             "data": "synthetic",
             "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": seed_of(cfg),
                        "ms_per_matrix": ms, "parallelism": (f"columns sharded x{world}" if colshard else f"rows sharded x{world}") if world > 1 else "single GPU",
@@ -496,7 +497,7 @@ def main():
                           "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                           "kernel": "dgemm_tc<128,128,64,32,6,K-major,K-major> (a7 G+ = X G')",
                           "flops_per_launch": out_flops_launch, "ms_per_launch": out_ms,
-                          "measured": roof_note, "peak_source": peak_src} if not args.emulate else
+                          "measured": roof_note, "peak_source": peak_src} if not (args.emulate and not tr) else
                          {"bound": "tensor", "achieved": achieved * 36 if achieved else None, "peak": 4500.0,
                           "unit": "TOPS (int8)", "frac": achieved * 36 / 4500.0 if achieved else None,
                           "traffic": None,
