@@ -479,7 +479,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if not args.emulate else
             ("f64 (Gram and a7 emulated on INT8 tensor cores: 8 int8 digits per element, 36 exact int32 digit "
-             "products, FP64 accumulation)" if not tr else "f64 (Gram emulated on INT8 tensor cores; a7 on DMMA)"),
+             "products, FP64 accumulation)" if s >= 3072 else "f64 (a7 emulated on INT8 tensor cores; Gram on DMMA)"),
             "data": "synthetic",
             "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": seed_of(cfg),
                        "ms_per_matrix": ms, "parallelism": (f"columns sharded x{world}" if colshard else f"rows sharded x{world}") if world > 1 else "single GPU",
@@ -497,11 +497,11 @@ def main():
                           "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                           "kernel": "dgemm_tc<128,128,64,32,6,K-major,K-major> (a7 G+ = X G')",
                           "flops_per_launch": out_flops_launch, "ms_per_launch": out_ms,
-                          "measured": roof_note, "peak_source": peak_src} if not (args.emulate and not tr) else
+                          "measured": roof_note, "peak_source": peak_src} if not args.emulate else
                          {"bound": "tensor", "achieved": achieved * 36 if achieved else None, "peak": 4500.0,
                           "unit": "TOPS (int8)", "frac": achieved * 36 / 4500.0 if achieved else None,
                           "traffic": None,
-                          "kernel": "emu_split + emu_gemm_kernel (a7 G+ = X G' as 36 int8 digit products, tcgen05.mma.kind::i8)",
+                          "kernel": "emu_split(_cols) + emu_gemm_kernel (a7 G+ = X G' / G' X as 36 int8 digit products, tcgen05.mma.kind::i8)",
                           "fp64_equivalent_tflops": achieved, "flops_per_launch": out_flops_launch,
                           "ms_per_launch": out_ms, "measured": roof_note + "; the a7 step = digit split of X and G + "
                           "the emulated products", "peak_source": "nominal B200 dense INT8 4.5 POPS (no measured int8 "

@@ -639,11 +639,42 @@ geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long
   return flag ? GENINV_ERANGE : GENINV_OK;
 }
 
+// a7 (T branch, m < n) on the INT8 tensor cores: Gp (n x m) = G' X, i.e. C[i][j] = sum_k G[k][i] X[j][k]:
+// digit planes of the COLUMNS of G (K = s = m rows, chunks of the n columns) against those of X.
+geninv_status apply_emulated_t(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
+                               long long ldp, cudaStream_t st) {
+  constexpr int S = 8, T = 9;
+  const int s = (int)m, Kp = emu_kpad(s);
+  const long long chunk = std::max<long long>(256, std::min<long long>(n, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
+  const long long cmax = std::min<long long>(chunk, n);
+  GI_TRYS(grow(h->emu_x, h->emu_x_bytes, (size_t)S * s * Kp));
+  GI_TRYS(grow(h->emu_ex, h->emu_ex_n, (size_t)s));
+  GI_TRYS(grow(h->emu_g, h->emu_g_bytes, (size_t)S * cmax * Kp));
+  GI_TRYS(grow(h->emu_eg, h->emu_eg_n, (size_t)cmax));
+  GI_TRYS(grow(h->emu_cm, h->emu_cm_n, (size_t)cmax));
+  GI_TRYS(grow(h->emu_sc, h->emu_sc_n, (size_t)emu_scratch_elems((int)cmax, s)));
+  if (!h->emu_flag) GI_TRY(cudaMalloc(&h->emu_flag, sizeof(int)));
+  GI_TRY(cudaMemsetAsync(h->emu_flag, 0, sizeof(int), st));
+  GI_TRY(emu_split(h->X, h->ld, s, s, S, h->emu_x, h->emu_ex, h->emu_flag, st));
+  h->launches += 1;
+  for (long long i0 = 0; i0 < n; i0 += chunk) {
+    const int nc = (int)std::min<long long>(chunk, n - i0);
+    GI_TRY(emu_split_cols(G + i0, ld, s, nc, S, h->emu_g, h->emu_eg, h->emu_cm, h->emu_flag, st));
+    GI_TRY(emu_gemm_nt(h->emu_g, h->emu_eg, nc, h->emu_x, h->emu_ex, s, s, S, T, Gp + i0 * ldp, ldp, h->emu_sc, st));
+    h->launches += 3;
+  }
+  int flag = 0;
+  GI_TRY(cudaMemcpyAsync(&flag, h->emu_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GI_TRY(cudaStreamSynchronize(st));
+  return flag ? GENINV_ERANGE : GENINV_OK;
+}
+
 geninv_status apply(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *Gp,
                     long long ldp, cudaStream_t st) {
   const long long s = trans ? m : n;
-  if (!trans && emulation_on(h) && s <= 16384) {
-    const geninv_status es = apply_emulated(h, G, m, n, ld, Gp, ldp, st);
+  if (emulation_on(h) && s <= 16384) {
+    const geninv_status es = trans ? apply_emulated_t(h, G, m, n, ld, Gp, ldp, st)
+                                   : apply_emulated(h, G, m, n, ld, Gp, ldp, st);
     if (es != GENINV_ERANGE) return es;   // out of the emulation's range: the native product below
   }
   GemmOp op;

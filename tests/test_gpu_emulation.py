@@ -4,7 +4,7 @@ residuals <= 1e-10 on inputs in Q) on ragged shapes -- M, N, K off the 128 / 256
 grid, K not a multiple of 16 (padded slices), several G chunks -- and agreement with the native
 FP64 tensor-core path within the summation-order noise of the chain (1e-10, as the schedule variants
 of tests/test_gpu_variants.py; the emulated products' own error bound is below an FP64 GEMM's).
-The Gram is emulated from s >= 3072 (test_emulated_gram_c3t), a7 on every N-branch shape."""
+The Gram is emulated from s >= 3072 (test_emulated_gram_c3t), a7 on every shape of both branches."""
 import numpy as np
 import pytest
 import torch
@@ -41,7 +41,8 @@ def penrose(G, X):
 
 
 @pytest.mark.parametrize("m,n,r", [(300, 140, 100), (1000, 333, 260), (2050, 530, 400), (700, 200, 200),
-                                   (4100, 129, 120), (1500, 1024, 1024)])
+                                   (4100, 129, 120), (1500, 1024, 1024),
+                                   (140, 300, 100), (333, 1000, 260), (530, 2050, 400), (129, 4100, 120)])
 def test_emulated_matches_oracle(H, m, n, r):
     G = I.low_rank(m * 7 + n, m, n, r).numpy() if r < n else I.dense_normal(m * 7 + n, m, n).numpy()
     R = O.geninv(G)
@@ -86,6 +87,20 @@ def test_emulated_gram_c3t(H):
     Gh = G.cpu().numpy()
     R = O.geninv(Gh)
     assert R.in_Q()
+    assert info.rank == R.rank == 3072
+    assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
+    assert max(penrose(Gh, Gp.cpu().numpy())) <= 1e-10
+
+
+def test_emulated_c3_t_branch(H):
+    """C3 (4096 x 16384, T branch): the Gram from row digit planes, a7 = G' X from column digit planes."""
+    G = I.make_single(I.CONFIGS["C3"], I.QSEED["C3"], device="cuda")
+    H.set_emulation(1)
+    Gp, info = H.geninv_d(G)
+    H.set_emulation(0)
+    Gh = G.cpu().numpy()
+    R = O.geninv(Gh)
+    assert R.in_Q() and info.transposed
     assert info.rank == R.rank == 3072
     assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
     assert max(penrose(Gh, Gp.cpu().numpy())) <= 1e-10
