@@ -274,10 +274,15 @@ __global__ void emu_split_kernel(const double *__restrict__ X, long long ldx, in
   const double inv = ldexp(1.0, -e);
   const long long plane = (long long)rows * Kp;
   int8_t *out = sl + (long long)warp * Kp;
+  bool bad = false;   // NaN / Inf: fmax above ignores NaN, so every element is checked here
   for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
     double v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = (k0 + q < K) ? x[k0 + q] * inv : 0.0;
+    for (int q = 0; q < 4; ++q) {
+      const double xv = (k0 + q < K) ? x[k0 + q] : 0.0;
+      bad |= !isfinite(xv);
+      v[q] = xv * inv;
+    }
     for (int t = 0; t < S; ++t) {
       char4 c;
       signed char d[4];
@@ -294,6 +299,7 @@ __global__ void emu_split_kernel(const double *__restrict__ X, long long ldx, in
         for (int q = 0; q < 4 && k0 + q < Kp; ++q) out[t * plane + k0 + q] = d[q];
     }
   }
+  if (bad) atomicOr(flag, 1);
 }
 
 // Column maxima of |G| over rows [0, rows) of a row-major block (the N-branch Gram's K-chunk):
@@ -346,8 +352,13 @@ __global__ void __launch_bounds__(256) emu_split_cols_kernel(const double *__res
     const double inv = ldexp(1.0, -e);
     const int k = r0 + 4 * lane;
     double v[4];
+    bool bad = false;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = t[cc][4 * lane + q] * inv;
+    for (int q = 0; q < 4; ++q) {
+      bad |= !isfinite(t[cc][4 * lane + q]);
+      v[q] = t[cc][4 * lane + q] * inv;
+    }
+    if (bad) atomicOr(flag, 1);
     int8_t *out = sl + (long long)c * Kp;
     for (int tt = 0; tt < S; ++tt) {
       signed char d[4];

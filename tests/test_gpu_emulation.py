@@ -104,3 +104,30 @@ def test_emulated_c3_t_branch(H):
     assert info.rank == R.rank == 3072
     assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
     assert max(penrose(Gh, Gp.cpu().numpy())) <= 1e-10
+
+
+@pytest.mark.parametrize("scale", [1e-150, 1e150])
+def test_emulated_extreme_scales(H, scale):
+    G0 = I.low_rank(31, 300, 140, 100).numpy()
+    R = O.geninv(G0)
+    H.set_emulation(1)
+    Gp, info = H.geninv_d(dev(G0 * scale))
+    H.set_emulation(0)
+    assert info.rank == R.rank
+    assert C.rel_fro(Gp.cpu().numpy() * scale, R.Gp) <= 1e-9
+
+
+def test_emulated_nonfinite_and_zero(H):
+    from paper_0804_4809_b200.binding import GENINV_ENONFINITE, GeninvError
+    G = I.dense_normal(3, 4000, 3100).numpy()        # s >= 3072: the emulated Gram path
+    G[17, 5] = np.nan
+    H.set_emulation(1)
+    try:
+        with pytest.raises(GeninvError) as exc:
+            H.geninv_d(dev(G))
+        assert exc.value.status == GENINV_ENONFINITE
+        Z = torch.zeros(400, 130, dtype=torch.float64, device="cuda")
+        Gp, info = H.geninv_d(Z)
+        assert info.rank == 0 and not Gp.any()
+    finally:
+        H.set_emulation(0)
