@@ -1,7 +1,8 @@
 """Parity report over the BASELINE configs (`-m gpu`, slow): one JSON record per config with the
 device and oracle ranks, pivot agreement, the oracle's decision margins (predicate Q, SURVEY
 §8(c4)), the relative difference of G+ and the four relative Penrose residuals (cuBLAS checker,
-test-only), and the device / oracle times -- the row SURVEY §8(d2) asks for.  Gates as in the
+test-only), and the device / oracle times -- the row SURVEY §8(d2) asks for -- for the native path
+and with the Gram / a7 emulated on the INT8 tensor cores.  Gates as in the
 other parity tests.  With GENINV_PARITY_REPORT=<path> the records are written there (JSON lines).
 C4 at full size is covered by tests/test_gpu_c4_full.py."""
 import json
@@ -52,8 +53,9 @@ def time_device(H, G, Gp, reps=5):
     return float(np.median(ts))
 
 
+@pytest.mark.parametrize("emulate", [0, 1], ids=["dmma", "int8_emulated"])
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C3T"])
-def test_config_parity_record(H, name):
+def test_config_parity_record(H, name, emulate):
     if name == "C3T":
         G = I.make_single(I.CONFIGS["C3"], I.QSEED["C3"], device="cuda").T.contiguous()
         seed = I.QSEED["C3"]
@@ -61,8 +63,10 @@ def test_config_parity_record(H, name):
         seed = I.QSEED[name]
         G = I.make_single(I.CONFIGS[name], seed, device="cuda")
     m, n = G.shape
+    H.set_emulation(emulate)
     Gp, info = H.geninv_d(G)
     ms = time_device(H, G, Gp)
+    H.set_emulation(0)
     Gh = G.cpu().numpy()
     t0 = time.perf_counter()
     R = O.geninv(Gh)
@@ -73,7 +77,8 @@ def test_config_parity_record(H, name):
     _, piv, _ = H.geninv_frchol_d(A)
     rel = C.rel_fro(Gp.cpu().numpy(), R.Gp)
     rh = rho(G, Gp)
-    rec = {"config": name, "seed": seed, "m": m, "n": n, "r_gpu": info.rank, "r_oracle": R.rank,
+    rec = {"config": name, "emulated": bool(emulate), "seed": seed, "m": m, "n": n, "r_gpu": info.rank,
+           "r_oracle": R.rank,
            "piv_equal": bool(np.array_equal(piv.cpu().numpy(), R.chol.piv)), "mu_acc": R.mu_acc,
            "mu_drop": R.mu_drop, "in_Q": R.in_Q(), "rel_fro": rel, "rho": rh, "device_ms": ms,
            "oracle_ms": oracle_ms, "oracle_threads": os.cpu_count()}
