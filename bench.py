@@ -483,7 +483,13 @@ def main():
             "data": "synthetic",
             "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": seed_of(cfg),
                        "ms_per_matrix": ms, "parallelism": (f"columns sharded x{world}" if colshard else f"rows sharded x{world}") if world > 1 else "single GPU",
-                       "pct_fp64_peak": value / (peak * 1e3), "flops_per_step": F["total"],
+                       "pct_fp64_peak": value / (peak * 1e3),
+                       "pct_fp64_peak_nominal_at_run_clock": (value / (148 * 128 * clocks["sm_mhz"] * 1e-3)
+                                                             if clocks.get("sm_mhz") else None),
+                       "pct_fp64_peak_note": "pct_fp64_peak: the measured DMMA peak (profiles/MEASURED_FP64.json); "
+                                             "nominal: 148 SM x 128 flop/clk x the SM clock sampled during the run; "
+                                             "no vendor FP64 figure is available offline",
+                       "flops_per_step": F["total"],
                        "phase_ms_rank0": phases,
                        "flops_breakdown": {k: v for k, v in F.items() if k != "total"},
                        "l2": "inputs (G 64 GiB) far larger than the 126 MB L2; no flush needed"
