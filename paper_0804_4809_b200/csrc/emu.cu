@@ -1,20 +1,22 @@
-// a7 on the INT8 tensor cores (opt-in: geninv_set_emulation): the FP64 product
-// C = X G' emulated by Ozaki splitting (DESIGN.md §6 "FP64 emulation").
+// The two big FP64 contractions (a1 Gram, a7 output product) on the INT8 tensor cores (SURVEY §8(f)
+// f4, opt-in: geninv_set_emulation; DESIGN.md §6 "FP64 emulation"), by Ozaki splitting.
 //
-// Every row of X (and of G) is scaled by a power of two 2^e (|x| 2^-e <= 127/128) and split into S
-// int8 digits, x = 2^e sum_{t=1..S} d_t 2^-7t + r with |r| <= 2^(e - 7S - 1) (error-free: each step
-// y = 128 v, d = rint(y), v = y - d is exact in FP64).  Then
-//   C[i][j] = 2^(e_i + f_j) sum_g 2^-7g P_g[i][j],  P_g = sum_{t+u=g} sum_k d_t[i][k] d'_u[j][k]
-// with every P_g an exact int32 sum (|P_g| <= S K 127^2 < 2^31 for K < 16384) computed by
+// Every line (row or column, whichever runs along K) of both operands is scaled by a power of two 2^e
+// (|x| 2^-e <= 127/128) and split into S int8 digits, x = 2^e sum_{t=1..S} d_t 2^-7t + r with
+// |r| <= 2^(e - 7S - 1) (error-free: each step y = 128 v, d = rint(y), v = y - d is exact in FP64).
+// Then C[i][j] = 2^(e_i + f_j) sum_g 2^-7g P_g[i][j],  P_g = sum_{t+u=g} sum_k d_t[i][k] d'_u[j][k],
+// every P_g an exact int32 sum (|P_g| <= 8 K 127^2 < 2^31 for K <= 16384) computed by
 // tcgen05.mma.kind::i8 into TMEM.  Groups g = T .. 2 (smallest terms first) are converted exactly to
-// FP64, scaled exactly (powers of two) and accumulated into C in FP64.  S = 8, T = 9 (36 int8
-// products) leaves |C - C_exact| <~ 4e-17 sum_k |x_ik g_jk| (tools/emu_gemm.cu), i.e. below an FP64
-// GEMM's own rounding bound.
+// FP64, scaled exactly (powers of two) and accumulated in FP64.  S = 8, T = 9 (36 int8 products)
+// leaves |C - C_exact| <~ 4e-17 sum_k |x_ik g_jk| (tools/emu_gemm.cu): below an FP64 GEMM's own
+// rounding bound.
 //
-// Kernel layout (one 128 x 256 tile of C per CTA, 192 threads): warp 0 lane 0 issues the TMA loads
-// (128-byte K slabs of the slice arrays, SWIZZLE_128B, 4-stage ring), warp 1 lane 0 issues the MMAs
-// (M = 128, N = 256, K = 32) into one of two TMEM accumulators (2 x 256 columns, ping-pong by group),
-// warps 2-5 (one TMEM lane quarter each) drain a finished group into C while the next one runs.
+// emu_gemm_kernel (persistent, 192 threads, one 128 x 256 tile of C at a time): warp 0 lane 0 issues
+// the TMA loads (128-byte K slabs of the digit planes, SWIZZLE_128B, 4-stage ring), warp 1 lane 0
+// issues the MMAs (M = 128, N = 256, K = 32) into one of two TMEM accumulators (2 x 256 columns,
+// ping-pong by group), warps 2-5 (one TMEM lane quarter each) drain a finished group into the
+// running sum while the next one runs.  The digit splits: emu_split_kernel (rows, K-major already),
+// emu_colmax_kernel + emu_split_cols_kernel (columns: a shared-memory transpose).
 #include <cudaTypedefs.h>
 #include <stdio.h>
 
