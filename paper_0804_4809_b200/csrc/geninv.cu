@@ -183,13 +183,25 @@ geninv_status grow(T *&p, size_t &have, size_t need) {
   return GENINV_OK;
 }
 
+// Largest digit group t + u of the emulated products: 9 (36 products, FP64-level); GENINV_EMU_T
+// (2 .. 16) trades accuracy for work in measurements.
+int emu_groups() {
+  static const int T = [] {
+    const char *e = getenv("GENINV_EMU_T");
+    const int t = e ? atoi(e) : 9;
+    return t >= 2 && t <= 16 ? t : 9;
+  }();
+  return T;
+}
+
 // a1 on the INT8 tensor cores (geninv_set_emulation): K-chunks of <= 16384 lines of G (the int32
 // group sums stay exact), each split into 8 int8 digits per column (N) / row (T) of the chunk, the
 // lower tiles of A accumulated chunk after chunk in FP64 (fixed order: deterministic).  GENINV_ERANGE:
 // a line outside the exact-scaling range (the caller then runs the DMMA Gram).
 geninv_status gram_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans,
                             double *A, long long lda, bool accumulate) {
-  constexpr int S = 8, T = 9, KC = 16384;
+  constexpr int S = 8, KC = 16384;
+  const int T = emu_groups();
   const long long s = trans ? m : n, ell = trans ? n : m;
   const int Kp = emu_kpad(KC);
   GI_TRYS(grow(h->emu_g, h->emu_g_bytes, (size_t)S * s * Kp));
@@ -608,11 +620,7 @@ geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n
 // row of X or G is outside the exact power-of-two scaling range; the caller then uses DMMA.
 geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
                              long long ldp, cudaStream_t st) {
-  static const int T = [] {
-    const char *e = getenv("GENINV_EMU_T");
-    const int t = e ? atoi(e) : 9;
-    return t >= 2 && t <= 16 ? t : 9;
-  }();
+  const int T = emu_groups();
   constexpr int S = 8;
   const int s = (int)n, Kp = emu_kpad(s);
   const long long chunk = std::max<long long>(256, std::min<long long>(m, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
@@ -643,7 +651,8 @@ geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long
 // digit planes of the COLUMNS of G (K = s = m rows, chunks of the n columns) against those of X.
 geninv_status apply_emulated_t(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
                                long long ldp, cudaStream_t st) {
-  constexpr int S = 8, T = 9;
+  constexpr int S = 8;
+  const int T = emu_groups();
   const int s = (int)m, Kp = emu_kpad(s);
   const long long chunk = std::max<long long>(256, std::min<long long>(n, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
   const long long cmax = std::min<long long>(chunk, n);
