@@ -2,14 +2,17 @@
 // f4, opt-in: geninv_set_emulation; DESIGN.md §6 "FP64 emulation"), by Ozaki splitting.
 //
 // Every line (row or column, whichever runs along K) of both operands is scaled by a power of two 2^e
-// (|x| 2^-e <= 127/128) and split into S int8 digits, x = 2^e sum_{t=1..S} d_t 2^-7t + r with
-// |r| <= 2^(e - 7S - 1) (error-free: each step y = 128 v, d = rint(y), v = y - d is exact in FP64).
-// Then C[i][j] = 2^(e_i + f_j) sum_g 2^-7g P_g[i][j],  P_g = sum_{t+u=g} sum_k d_t[i][k] d'_u[j][k],
-// every P_g an exact int32 sum (|P_g| <= 8 K 127^2 < 2^31 for K <= 16384) computed by
-// tcgen05.mma.kind::i8 into TMEM.  Groups g = T .. 2 (smallest terms first) are converted exactly to
-// FP64, scaled exactly (powers of two) and accumulated in FP64.  S = 8, T = 9 (36 int8 products)
-// leaves |C - C_exact| <~ 4e-17 sum_k |x_ik g_jk| (tools/emu_gemm.cu): below an FP64 GEMM's own
-// rounding bound.
+// (|x| < 2^e) and split error-free into S digits with weights w_t = 2^(1-8t):
+//   v = x 2^-e in (-1, 1):  d_1 = floor(128 v) in [-128, 127] (signed int8),  v <- 128 v - d_1 in [0, 1);
+//   t >= 2:                 d_t = floor(256 v) in [0, 255]   (unsigned int8), v <- 256 v - d_t,
+// every step exact in FP64, so x = 2^e sum_t d_t w_t + r with 0 <= r 2^-e < 2^(1-8S).  Then
+//   C[i][j] = 2^(e_i + f_j) sum_g 2^(2-8g) P_g[i][j],  P_g = sum_{t+u=g} sum_k d_t[i][k] d'_u[j][k],
+// every P_g an exact int32 sum (at most 7 pairs x K x 255^2 < 2^31 for K <= 4096 per pass) computed by
+// tcgen05.mma.kind::i8 with each operand's signedness set per digit (d_1 signed, the rest unsigned).
+// Groups g = T .. 2 (smallest terms first) are converted exactly to FP64, scaled exactly (powers of
+// two) and accumulated in FP64.  S = 7, T = 9 (34 int8 products) leaves |C - C_exact| <= 2.4e-17
+// sum_k |x_ik g_jk| (tools/emu_gemm.cu against a long-double reference): below an FP64 GEMM's own
+// rounding bound.  (T = 8, 28 products: 2.9e-15 -- the unsigned digits' errors do not cancel.)
 //
 // emu_gemm_kernel (persistent, 192 threads, one 128 x 256 tile of C at a time): warp 0 lane 0 issues
 // the TMA loads (128-byte K slabs of the digit planes, SWIZZLE_128B, 4-stage ring), warp 1 lane 0
@@ -34,8 +37,11 @@ constexpr int EBM = 128, EBN = 256, EBK = 128, ESTAGES = 4;
 constexpr int EA_BYTES = EBM * EBK, EB_BYTES = EBN * EBK, ESTAGE_BYTES = EA_BYTES + EB_BYTES;
 constexpr int ESMEM = ESTAGES * ESTAGE_BYTES + 1024 + 512 + EBN * 4;
 constexpr int ENT = 192;
-constexpr uint32_t IDESC_I8 =
-    (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(EBN >> 3) << 17) | ((uint32_t)(EBM >> 4) << 24);
+// kind::i8 instruction descriptor: D s32, K-major A and B, N = 256, M = 128; A / B signed (1) or not (0)
+GI_DEV uint32_t idesc_i8(int a_signed, int b_signed) {
+  return (2u << 4) | ((uint32_t)a_signed << 7) | ((uint32_t)b_signed << 10) | ((uint32_t)(EBN >> 3) << 17) |
+         ((uint32_t)(EBM >> 4) << 24);
+}
 
 GI_DEV void tma_load_3d_u8(void *dst, const CUtensorMap *m, uint64_t *bar, int c0, int c1, int c2) {
   tma_load_3d(dst, m, bar, c0, c1, c2);
@@ -49,11 +55,11 @@ GI_DEV uint64_t umma_desc(uint32_t addr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-GI_DEV void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+GI_DEV void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(IDESC_I8), "r"(acc));
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 GI_DEV void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -156,7 +162,8 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t acc = tmem + buf * EBN;
           uint32_t accumulate = 0;
-          for (int t = max(1, g - S); t <= min(S, g - 1); ++t)
+          for (int t = max(1, g - S); t <= min(S, g - 1); ++t) {
+            const uint32_t idesc = idesc_i8(t == 1, g - t == 1);   // d_1 signed, later digits unsigned
             for (int kb = 0; kb < nk; ++kb, ++it) {
               const int st = it % ESTAGES;
               mbar_wait(&full[st], (it / ESTAGES) & 1);
@@ -164,11 +171,12 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
               const uint32_t a0 = smem_u32(smem + st * ESTAGE_BYTES), b0 = a0 + EA_BYTES;
 #pragma unroll
               for (int kk = 0; kk < EBK / 32; ++kk) {
-                mma_i8(acc, umma_desc(a0 + 32 * kk), umma_desc(b0 + 32 * kk), accumulate);
+                mma_i8(acc, umma_desc(a0 + 32 * kk), umma_desc(b0 + 32 * kk), idesc, accumulate);
                 accumulate = 1;
               }
               mma_commit(&empty[st]);   // the stage is free once these MMAs have read it
             }
+          }
           mma_commit(&accfull[buf]);
         }
     }
@@ -193,7 +201,7 @@ __global__ void __launch_bounds__(ENT, 1) emu_gemm_kernel(const __grid_constant_
         const bool first = g == T, last = g == 2;
         mbar_wait(&accfull[buf], (q >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const double sr = pow2i(ea_r - 7 * g);
+        const double sr = pow2i(ea_r + 2 - 8 * g);   // the group's digit weight 2^(2-8g)
         for (int c0 = 0; c0 < EBN; c0 += 32) {
           uint32_t r[32];
           asm volatile(
@@ -264,10 +272,7 @@ __global__ void emu_split_kernel(const double *__restrict__ X, long long ldx, in
   for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(x[k]));
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   int e = 0;
-  if (mx > 0.0) {
-    frexp(mx * (128.0 / 127.0), &e);                // mx 128/127 < 2^e
-    if (!(mx * (128.0 / 127.0) < ldexp(1.0, e))) ++e;
-  }
+  if (mx > 0.0) frexp(mx, &e);                      // mx < 2^e
   if (!isfinite(mx) || e < -900 || e > 900) {
     if (lane == 0) atomicOr(flag, 1);
     e = 0;
@@ -290,9 +295,9 @@ __global__ void emu_split_kernel(const double *__restrict__ X, long long ldx, in
       signed char d[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double y = v[q] * 128.0;
-        const double r = rint(y);
-        d[q] = (signed char)(int)r;
+        const double y = v[q] * (t == 0 ? 128.0 : 256.0);
+        const double r = floor(y);                   // t = 0: [-128, 127]; later: [0, 255] (v >= 0)
+        d[q] = (signed char)(unsigned char)(int)r;
         v[q] = y - r;
       }
       c.x = d[0]; c.y = d[1]; c.z = d[2]; c.w = d[3];
@@ -318,10 +323,7 @@ __global__ void emu_colmax_kernel(const double *__restrict__ G, long long ld, in
 
 GI_DEV int emu_exponent(double mx, int *flag) {
   int e = 0;
-  if (mx > 0.0) {
-    frexp(mx * (128.0 / 127.0), &e);
-    if (!(mx * (128.0 / 127.0) < ldexp(1.0, e))) ++e;
-  }
+  if (mx > 0.0) frexp(mx, &e);                      // mx < 2^e
   if (!isfinite(mx) || e < -900 || e > 900) {
     atomicOr(flag, 1);
     e = 0;
@@ -366,9 +368,9 @@ __global__ void __launch_bounds__(256) emu_split_cols_kernel(const double *__res
       signed char d[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const double y = v[q] * 128.0;
-        const double rr = rint(y);
-        d[q] = (signed char)(int)rr;
+        const double y = v[q] * (tt == 0 ? 128.0 : 256.0);
+        const double rr = floor(y);
+        d[q] = (signed char)(unsigned char)(int)rr;
         v[q] = y - rr;
       }
       if (k + 3 < Kp) {

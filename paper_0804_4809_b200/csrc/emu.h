@@ -8,7 +8,8 @@ namespace gi {
 // K rounded up to 16 bytes (the slice arrays' row length; TMA needs 16-byte row strides).
 int emu_kpad(int K);
 
-// rows x K FP64 block (row stride ldx) -> S int8 digit slices [S][rows][emu_kpad(K)] and one
+// rows x K FP64 block (row stride ldx) -> S digit slices [S][rows][emu_kpad(K)] (digit 1 signed int8,
+// the others unsigned, see emu.cu) and one
 // power-of-two exponent per row; *flag |= 1 for a row outside the exact-scaling range.
 cudaError_t emu_split(const double *X, long long ldx, int rows, int K, int S, int8_t *slices, int *exps, int *flag,
                       cudaStream_t st);
@@ -20,7 +21,7 @@ cudaError_t emu_split_cols(const double *G, long long ld, int rows, int cols, in
                            unsigned long long *colmax, int *flag, cudaStream_t st);
 
 // C (M x N, row stride ldc) = A B' from the slices of A (M rows) and B (N rows) over K, groups
-// t + u <= T (S = 8, T = 9: 36 int8 products, FP64-level accuracy).  K <= 16384.  scratch: FP64
+// t + u <= T (S = 7, T = 9: 34 int8 products, FP64-level accuracy).  K <= 4096.  scratch: FP64
 // workspace of emu_scratch_elems(M, N) (the running sums, one tile per CTA).
 long long emu_scratch_elems(int M, int N);
 // lower: only the tiles of a square output's lower triangle (M == N); accumulate: C += A B'.

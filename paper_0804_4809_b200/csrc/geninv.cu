@@ -183,24 +183,27 @@ geninv_status grow(T *&p, size_t &have, size_t need) {
   return GENINV_OK;
 }
 
-// Largest digit group t + u of the emulated products: 9 (36 products, FP64-level); GENINV_EMU_T
-// (2 .. 16) trades accuracy for work in measurements.
+// Digits per line (7: 7 + 6 x 8 = 55 bits) and the largest digit group t + u of the emulated products
+// (9: 34 products, |error| <= 2.4e-17 sum |x g| measured -- FP64-level; 8: 28 products, 2.9e-15, too
+// coarse for the 1e-9 gate on C4); GENINV_EMU_T (2 .. 14) trades accuracy for work in measurements.
+constexpr int EMU_S = 7;
+constexpr int EMU_K = 4096;   // K per exact int32 pass: 7 pairs x 4096 x 255^2 < 2^31
 int emu_groups() {
   static const int T = [] {
     const char *e = getenv("GENINV_EMU_T");
     const int t = e ? atoi(e) : 9;
-    return t >= 2 && t <= 16 ? t : 9;
+    return t >= 2 && t <= 14 ? t : 9;
   }();
   return T;
 }
 
-// a1 on the INT8 tensor cores (geninv_set_emulation): K-chunks of <= 16384 lines of G (the int32
-// group sums stay exact), each split into 8 int8 digits per column (N) / row (T) of the chunk, the
+// a1 on the INT8 tensor cores (geninv_set_emulation): K-chunks of <= EMU_K lines of G (the int32
+// group sums stay exact), each split into EMU_S int8 digits per column (N) / row (T) of the chunk, the
 // lower tiles of A accumulated chunk after chunk in FP64 (fixed order: deterministic).  GENINV_ERANGE:
 // a line outside the exact-scaling range (the caller then runs the DMMA Gram).
 geninv_status gram_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans,
                             double *A, long long lda, bool accumulate) {
-  constexpr int S = 8, KC = 16384;
+  constexpr int S = EMU_S, KC = EMU_K;
   const int T = emu_groups();
   const long long s = trans ? m : n, ell = trans ? n : m;
   const int Kp = emu_kpad(KC);
@@ -232,7 +235,7 @@ geninv_status gram(geninv_handle h, const double *G, long long m, long long n, l
   const long long s = trans ? m : n, ell = trans ? n : m;
   // emulated Gram: only where its 128 x 256 lower tiles fill the machine (s >= 3072: >= 170 tiles);
   // an accumulating call could not fall back after a range flag
-  if (emulation_on(h) && !accumulate && s >= 3072 && s <= 16384) {
+  if (emulation_on(h) && !accumulate && s >= 3072 && s <= 16384) {   // K-chunks of EMU_K lines
     const geninv_status es = gram_emulated(h, G, m, n, ld, trans, A, lda, false);
     if (es != GENINV_ERANGE) return es;   // out of the emulation's range: the DMMA Gram below
   }
@@ -621,7 +624,7 @@ geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n
 geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
                              long long ldp, cudaStream_t st) {
   const int T = emu_groups();
-  constexpr int S = 8;
+  constexpr int S = EMU_S;
   const int s = (int)n, Kp = emu_kpad(s);
   const long long chunk = std::max<long long>(256, std::min<long long>(m, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
   GI_TRYS(grow(h->emu_x, h->emu_x_bytes, (size_t)S * s * Kp));
@@ -651,7 +654,7 @@ geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long
 // digit planes of the COLUMNS of G (K = s = m rows, chunks of the n columns) against those of X.
 geninv_status apply_emulated_t(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
                                long long ldp, cudaStream_t st) {
-  constexpr int S = 8;
+  constexpr int S = EMU_S;
   const int T = emu_groups();
   const int s = (int)m, Kp = emu_kpad(s);
   const long long chunk = std::max<long long>(256, std::min<long long>(n, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
@@ -681,7 +684,7 @@ geninv_status apply_emulated_t(geninv_handle h, const double *G, long long m, lo
 geninv_status apply(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *Gp,
                     long long ldp, cudaStream_t st) {
   const long long s = trans ? m : n;
-  if (emulation_on(h) && s <= 16384) {
+  if (emulation_on(h) && s <= EMU_K) {   // one exact int32 pass over K = s
     const geninv_status es = trans ? apply_emulated_t(h, G, m, n, ld, Gp, ldp, st)
                                    : apply_emulated(h, G, m, n, ld, Gp, ldp, st);
     if (es != GENINV_ERANGE) return es;   // out of the emulation's range: the native product below

@@ -1,8 +1,8 @@
 // FP64 GEMM emulated on the INT8 tensor cores (Ozaki splitting; measurement / development tool for
 // SURVEY f4, not product code):  C (fp64, M x N) = A (fp64, M x K) * B (fp64, N x K)'.
-// Each row of A and of B is scaled by a power of two and split into S int8 slices,
-//   A[i][k] = 2^ea_i sum_t a_t[i][k] 2^-7t (+ residual),  B[j][k] = 2^eb_j sum_u b_u[j][k] 2^-7u,
-// so C[i][j] = 2^(ea_i + eb_j) sum_g 2^-7g P_g[i][j] with the exact int32 group sums
+// Each row of A and of B is scaled by a power of two and split into S digits with weights 2^(1-8t)
+// (the first signed, base 128; the others unsigned, base 256 -- the scheme of csrc/emu.cu), so
+// C[i][j] = 2^(ea_i + eb_j) sum_g 2^(2-8g) P_g[i][j] with the exact int32 group sums
 // P_g = sum_{t+u=g} a_t b_u' (tcgen05.mma.kind::i8, TMEM accumulators), groups g <= T.
 // The epilogue warps turn each group's int32 tile into fp64 (exact), scale it (exact power of two)
 // and accumulate it into C in global memory, largest g (smallest terms) first.
@@ -55,12 +55,15 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ uint32_t idesc_i8(int as, int bs) {
+  return (2u << 4) | ((uint32_t)as << 7) | ((uint32_t)bs << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(bar))
@@ -129,7 +132,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) emu_gemm(const __grid_constant__ 
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t acc = tmem + buf * BN;
         bool first = true;
-        for (int t = max(1, g - S); t <= min(S, g - 1); ++t)
+        for (int t = max(1, g - S); t <= min(S, g - 1); ++t) {
+          const uint32_t idesc = idesc_i8(t == 1, g - t == 1);
           for (int kb = 0; kb < nk; ++kb, ++it) {
             const int st = it % STAGES;
             mbar_wait(&full[st], (it / STAGES) & 1);
@@ -137,11 +141,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) emu_gemm(const __grid_constant__ 
             const uint32_t a0 = sa(smem + st * STAGE_BYTES), b0 = a0 + A_BYTES;
 #pragma unroll
             for (int kk = 0; kk < BK / 32; ++kk) {
-              mma_i8(acc, smem_desc(a0 + 32 * kk), smem_desc(b0 + 32 * kk), first ? 0u : 1u);
+              mma_i8(acc, smem_desc(a0 + 32 * kk), smem_desc(b0 + 32 * kk), idesc, first ? 0u : 1u);
               first = false;
             }
             mma_commit(&empty[st]);
           }
+        }
         mma_commit(&accfull[buf]);
       }
     }
@@ -172,8 +177,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) emu_gemm(const __grid_constant__ 
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             if (n0 + c0 + j + 1 < N + 1) {
-              const double v0 = (double)(int)r[j] * pow2(ea_r + s_eb[c0 + j] - 7 * g);
-              const double v1 = (double)(int)r[j + 1] * pow2(ea_r + s_eb[c0 + j + 1] - 7 * g);
+              const double v0 = (double)(int)r[j] * pow2(ea_r + s_eb[c0 + j] + 2 - 8 * g);
+              const double v1 = (double)(int)r[j + 1] * pow2(ea_r + s_eb[c0 + j + 1] + 2 - 8 * g);
               double2 *d2 = (double2 *)(dst + j);
               if (q == 0) {
                 *d2 = make_double2(v0, v1);
@@ -215,6 +220,8 @@ static CUtensorMap make_map(const int8_t *p, int rows, int K, int S, int box_row
 }
 
 // row-wise split of X (rows x K) into S int8 slices [S][rows][K] and exponents
+// row-wise split of X (rows x K) into S digit slices [S][rows][K] (digit 1 signed, base 128; later
+// digits unsigned, base 256: weights 2^(1-8t)) and exponents (max |x| < 2^e)
 static void split_host(const std::vector<double> &X, int rows, int K, int S, std::vector<int8_t> &sl,
                        std::vector<int> &e) {
   sl.assign((size_t)S * rows * K, 0);
@@ -223,17 +230,14 @@ static void split_host(const std::vector<double> &X, int rows, int K, int S, std
     double mx = 0;
     for (int k = 0; k < K; ++k) mx = std::max(mx, std::fabs(X[(size_t)i * K + k]));
     int ex = 0;
-    if (mx > 0) {
-      ex = (int)std::ceil(std::log2(mx * 128.0 / 127.0));
-      while (std::ldexp(mx, -ex) * 128.0 > 127.0) ++ex;
-    }
+    if (mx > 0) std::frexp(mx, &ex);
     e[i] = ex;
     for (int k = 0; k < K; ++k) {
       double v = std::ldexp(X[(size_t)i * K + k], -ex);
       for (int t = 0; t < S; ++t) {
-        const double y = v * 128.0;
-        const double d = std::nearbyint(y);
-        sl[((size_t)t * rows + i) * K + k] = (int8_t)d;
+        const double y = v * (t == 0 ? 128.0 : 256.0);
+        const double d = std::floor(y);
+        sl[((size_t)t * rows + i) * K + k] = (int8_t)(uint8_t)(int)d;
         v = y - d;
       }
     }
@@ -245,9 +249,9 @@ int main(int argc, char **argv) {
   void *fn = nullptr;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr);
   encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-  const int S = 8, T = argc > 1 ? atoi(argv[1]) : 9;
+  const int S = 7, T = argc > 1 ? atoi(argv[1]) : 9;
   for (int pass = 0; pass < 2; ++pass) {
-    const int M = pass ? 4096 : 256, N = pass ? (argc > 2 ? atoi(argv[2]) : 32768) : 512, K = pass ? 4096 : 1024;
+    const int M = pass ? 4096 : 256, N = pass ? (argc > 2 ? atoi(argv[2]) : 32768) : 512, K = pass ? 4096 : 4096;
     std::vector<double> A((size_t)M * K), B((size_t)N * K);
     unsigned s = 7;
     auto rnd = [&]() {
