@@ -39,6 +39,11 @@ FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "MEASURED_FP64.json")
 SEED = 1
 
 
+# digit products of the emulated contractions (csrc/emu.cu: 7 digits, groups t + u <= T, T = 9)
+_EMU_T = int(os.environ.get("GENINV_EMU_T", "9"))
+EMU_PAIRS = sum(1 for t in range(1, 8) for u in range(1, 8) if t + u <= _EMU_T)
+
+
 def seed_of(cfg) -> int:
     """The seed the parity tests use for this config (inputs.QSEED: the oracle's margins are in Q)."""
     return I.QSEED.get(cfg.name if cfg.name != "C3T" else "C3", SEED)
@@ -478,8 +483,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if not args.emulate else
-            ("f64 (Gram and a7 emulated on INT8 tensor cores: 8 int8 digits per element, 36 exact int32 digit "
-             "products, FP64 accumulation)" if s >= 3072 else "f64 (a7 emulated on INT8 tensor cores; Gram on DMMA)"),
+            (f"f64 (Gram and a7 emulated on INT8 tensor cores: 7 int8 digits per element, {EMU_PAIRS} exact int32 "
+             "digit products, FP64 accumulation)" if s >= 3072 else "f64 (a7 emulated on INT8 tensor cores; Gram on DMMA)"),
             "data": "synthetic",
             "config": {"workload": desc, "m": m, "n": n, "rank": rank_ok, "seed": seed_of(cfg),
                        "ms_per_matrix": ms, "parallelism": (f"columns sharded x{world}" if colshard else f"rows sharded x{world}") if world > 1 else "single GPU",
@@ -504,10 +509,10 @@ def main():
                           "kernel": "dgemm_tc<128,128,64,32,6,K-major,K-major> (a7 G+ = X G')",
                           "flops_per_launch": out_flops_launch, "ms_per_launch": out_ms,
                           "measured": roof_note, "peak_source": peak_src} if not args.emulate else
-                         {"bound": "tensor", "achieved": achieved * 36 if achieved else None, "peak": 4500.0,
-                          "unit": "TOPS (int8)", "frac": achieved * 36 / 4500.0 if achieved else None,
+                         {"bound": "tensor", "achieved": achieved * EMU_PAIRS if achieved else None, "peak": 4500.0,
+                          "unit": "TOPS (int8)", "frac": achieved * EMU_PAIRS / 4500.0 if achieved else None,
                           "traffic": None,
-                          "kernel": "emu_split(_cols) + emu_gemm_kernel (a7 G+ = X G' / G' X as 36 int8 digit products, tcgen05.mma.kind::i8)",
+                          "kernel": f"emu_split(_cols) + emu_gemm_kernel (a7 G+ = X G' / G' X as {EMU_PAIRS} int8 digit products, tcgen05.mma.kind::i8)",
                           "fp64_equivalent_tflops": achieved, "flops_per_launch": out_flops_launch,
                           "ms_per_launch": out_ms, "measured": roof_note + "; the a7 step = digit split of X and G + "
                           "the emulated products", "peak_source": "nominal B200 dense INT8 4.5 POPS (no measured int8 "
