@@ -94,10 +94,11 @@ GENINV_API geninv_status geninv_destroy(geninv_handle h);
 /* Arithmetic of the two big contractions (opt-in).  mode 0 (default): FP64 tensor
  * cores (DMMA).  mode 1: the output product (a7, both branches, X order) and the Gram (a1, s >= 3072;
  * not for geninv_host_d's accumulating chunks) emulated on the INT8 tensor cores (tcgen05.mma.kind::i8):
- * every line of the operands is scaled by a power of two and split into 8 int8 digits, the 36 digit
+ * every line of the operands is scaled by a power of two and split into 7 int8 digits, the 34 digit
  * products with t + u <= 9 are exact int32 sums in TMEM, accumulated in FP64 -- an error below
- * ~4e-17 sum_k |x_ik g_jk|, under an FP64 GEMM's own rounding bound.  For
- * s = min(m, n) <= 16384; lines outside 2^(+-900) fall back to DMMA.  Environment GENINV_EMULATE=1
+ * ~2.4e-17 sum_k |x_ik g_jk|, under an FP64 GEMM's own rounding bound.  a7 for
+ * s = min(m, n) <= 4096, the Gram for 3072 <= s <= 16384; lines outside 2^(+-900) or with NaN / Inf
+ * fall back to DMMA.  Environment GENINV_EMULATE=1
  * sets mode 1 for handles that never call this. */
 GENINV_API geninv_status geninv_set_emulation(geninv_handle h, int mode);
 GENINV_API const char *geninv_strerror(geninv_status st);
