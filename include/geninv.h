@@ -97,7 +97,7 @@ GENINV_API geninv_status geninv_destroy(geninv_handle h);
  * every line of the operands is scaled by a power of two and split into 7 int8 digits, the 34 digit
  * products with t + u <= 9 are exact int32 sums in TMEM, accumulated in FP64 -- an error below
  * ~2.4e-17 sum_k |x_ik g_jk|, under an FP64 GEMM's own rounding bound.  a7 for
- * s = min(m, n) <= 4096, the Gram for 3072 <= s <= 16384; lines outside 2^(+-900) or with NaN / Inf
+ * s = min(m, n) <= 16384, the Gram for 3072 <= s <= 16384; lines outside 2^(+-900) or with NaN / Inf
  * fall back to DMMA.  Environment GENINV_EMULATE=1
  * sets mode 1 for handles that never call this. */
 GENINV_API geninv_status geninv_set_emulation(geninv_handle h, int mode);

@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "../../include/geninv.h"
 #include "emu.h"
@@ -618,62 +619,57 @@ geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n
 }
 
 // a7: Gp = X G' (trans 0: Gp is n x m) or G' X (trans 1: Gp is n x m).
-// a7 (N branch) on the INT8 tensor cores: Gp (s x m) = X G' from S = 8 int8 slices of X and of
-// row chunks of G (Ozaki splitting, emu.cu).  Returns GENINV_ERANGE (nothing usable written) if a
-// row of X or G is outside the exact power-of-two scaling range; the caller then uses DMMA.
-geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
-                             long long ldp, cudaStream_t st) {
+// a7 on the INT8 tensor cores: N branch Gp (s x m) = X G', T branch Gp (n x m) = G' X, over K = s in
+// exact int32 passes of EMU_K (each pass has its own per-line exponents, the passes add up in FP64).
+// The digit planes of X for every pass are made once; G is taken in chunks of its long side (rows
+// for N, columns for T: those are the lines of G' X).  Returns GENINV_ERANGE (nothing usable written)
+// for a line outside the exact-scaling range or with NaN / Inf; the caller then uses DMMA.
+geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans,
+                             double *Gp, long long ldp, cudaStream_t st) {
   const int T = emu_groups();
   constexpr int S = EMU_S;
-  const int s = (int)n, Kp = emu_kpad(s);
-  const long long chunk = std::max<long long>(256, std::min<long long>(m, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
-  GI_TRYS(grow(h->emu_x, h->emu_x_bytes, (size_t)S * s * Kp));
-  GI_TRYS(grow(h->emu_ex, h->emu_ex_n, (size_t)s));
-  GI_TRYS(grow(h->emu_g, h->emu_g_bytes, (size_t)S * std::min<long long>(chunk, m) * Kp));
-  GI_TRYS(grow(h->emu_eg, h->emu_eg_n, (size_t)std::min<long long>(chunk, m)));
-  GI_TRYS(grow(h->emu_sc, h->emu_sc_n, (size_t)emu_scratch_elems(s, (int)std::min<long long>(chunk, m))));
-  if (!h->emu_flag) {
-    GI_TRY(cudaMalloc(&h->emu_flag, sizeof(int)));
-  }
-  GI_TRY(cudaMemsetAsync(h->emu_flag, 0, sizeof(int), st));
-  GI_TRY(emu_split(h->X, h->ld, s, s, S, h->emu_x, h->emu_ex, h->emu_flag, st));
-  h->launches += 1;
-  for (long long j0 = 0; j0 < m; j0 += chunk) {
-    const int nc = (int)std::min<long long>(chunk, m - j0);
-    GI_TRY(emu_split(G + j0 * ld, ld, nc, s, S, h->emu_g, h->emu_eg, h->emu_flag, st));
-    GI_TRY(emu_gemm_nt(h->emu_x, h->emu_ex, s, h->emu_g, h->emu_eg, nc, s, S, T, Gp + j0, ldp, h->emu_sc, st));
-    h->launches += 2;
-  }
-  int flag = 0;
-  GI_TRY(cudaMemcpyAsync(&flag, h->emu_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  GI_TRY(cudaStreamSynchronize(st));
-  return flag ? GENINV_ERANGE : GENINV_OK;
-}
-
-// a7 (T branch, m < n) on the INT8 tensor cores: Gp (n x m) = G' X, i.e. C[i][j] = sum_k G[k][i] X[j][k]:
-// digit planes of the COLUMNS of G (K = s = m rows, chunks of the n columns) against those of X.
-geninv_status apply_emulated_t(geninv_handle h, const double *G, long long m, long long n, long long ld, double *Gp,
-                               long long ldp, cudaStream_t st) {
-  constexpr int S = EMU_S;
-  const int T = emu_groups();
-  const int s = (int)m, Kp = emu_kpad(s);
-  const long long chunk = std::max<long long>(256, std::min<long long>(n, (2LL << 30) / ((long long)S * Kp)) / 256 * 256);
-  const long long cmax = std::min<long long>(chunk, n);
-  GI_TRYS(grow(h->emu_x, h->emu_x_bytes, (size_t)S * s * Kp));
-  GI_TRYS(grow(h->emu_ex, h->emu_ex_n, (size_t)s));
-  GI_TRYS(grow(h->emu_g, h->emu_g_bytes, (size_t)S * cmax * Kp));
+  const int s = (int)(trans ? m : n);
+  const long long ell = trans ? n : m;
+  const int npass = (s + EMU_K - 1) / EMU_K;
+  long long xplanes = 0;   // bytes of X's digit planes over all passes
+  for (int p = 0; p < npass; ++p) xplanes += (long long)S * s * emu_kpad(std::min(EMU_K, s - p * EMU_K));
+  const int Kp1 = emu_kpad(std::min(EMU_K, s));
+  const long long chunk =
+      std::max<long long>(256, std::min<long long>(ell, (2LL << 30) / ((long long)S * Kp1)) / 256 * 256);
+  const long long cmax = std::min<long long>(chunk, ell);
+  GI_TRYS(grow(h->emu_x, h->emu_x_bytes, (size_t)xplanes));
+  GI_TRYS(grow(h->emu_ex, h->emu_ex_n, (size_t)s * npass));
+  GI_TRYS(grow(h->emu_g, h->emu_g_bytes, (size_t)S * cmax * Kp1));
   GI_TRYS(grow(h->emu_eg, h->emu_eg_n, (size_t)cmax));
   GI_TRYS(grow(h->emu_cm, h->emu_cm_n, (size_t)cmax));
-  GI_TRYS(grow(h->emu_sc, h->emu_sc_n, (size_t)emu_scratch_elems((int)cmax, s)));
+  GI_TRYS(grow(h->emu_sc, h->emu_sc_n,
+               (size_t)std::max(emu_scratch_elems(s, (int)cmax), emu_scratch_elems((int)cmax, s))));
   if (!h->emu_flag) GI_TRY(cudaMalloc(&h->emu_flag, sizeof(int)));
   GI_TRY(cudaMemsetAsync(h->emu_flag, 0, sizeof(int), st));
-  GI_TRY(emu_split(h->X, h->ld, s, s, S, h->emu_x, h->emu_ex, h->emu_flag, st));
-  h->launches += 1;
-  for (long long i0 = 0; i0 < n; i0 += chunk) {
-    const int nc = (int)std::min<long long>(chunk, n - i0);
-    GI_TRY(emu_split_cols(G + i0, ld, s, nc, S, h->emu_g, h->emu_eg, h->emu_cm, h->emu_flag, st));
-    GI_TRY(emu_gemm_nt(h->emu_g, h->emu_eg, nc, h->emu_x, h->emu_ex, s, s, S, T, Gp + i0 * ldp, ldp, h->emu_sc, st));
-    h->launches += 3;
+  std::vector<long long> xoff(npass + 1, 0);
+  for (int p = 0; p < npass; ++p) {
+    const int k0 = p * EMU_K, kw = std::min(EMU_K, s - k0);
+    xoff[p + 1] = xoff[p] + (long long)S * s * emu_kpad(kw);
+    GI_TRY(emu_split(h->X + k0, h->ld, s, kw, S, h->emu_x + xoff[p], h->emu_ex + (long long)p * s, h->emu_flag, st));
+    h->launches += 1;
+  }
+  for (long long j0 = 0; j0 < ell; j0 += chunk) {
+    const int nc = (int)std::min<long long>(chunk, ell - j0);
+    for (int p = 0; p < npass; ++p) {
+      const int k0 = p * EMU_K, kw = std::min(EMU_K, s - k0);
+      const int8_t *xs = h->emu_x + xoff[p];
+      const int *xe = h->emu_ex + (long long)p * s;
+      if (!trans) {   // lines of G = its rows j0 .., K columns k0 ..;  C[i][j] = sum_k X[i][k] G[j][k]
+        GI_TRY(emu_split(G + j0 * ld + k0, ld, nc, kw, S, h->emu_g, h->emu_eg, h->emu_flag, st));
+        GI_TRY(emu_gemm_nt(xs, xe, s, h->emu_g, h->emu_eg, nc, kw, S, T, Gp + j0, ldp, h->emu_sc, st, 0, p > 0));
+        h->launches += 2;
+      } else {        // lines of G' = columns j0 .. of G, K rows k0 ..;  C[i][j] = sum_k G[k][i] X[j][k]
+        GI_TRY(emu_split_cols(G + (long long)k0 * ld + j0, ld, kw, nc, S, h->emu_g, h->emu_eg, h->emu_cm, h->emu_flag,
+                              st));
+        GI_TRY(emu_gemm_nt(h->emu_g, h->emu_eg, nc, xs, xe, s, kw, S, T, Gp + j0 * ldp, ldp, h->emu_sc, st, 0, p > 0));
+        h->launches += 3;
+      }
+    }
   }
   int flag = 0;
   GI_TRY(cudaMemcpyAsync(&flag, h->emu_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -684,9 +680,8 @@ geninv_status apply_emulated_t(geninv_handle h, const double *G, long long m, lo
 geninv_status apply(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *Gp,
                     long long ldp, cudaStream_t st) {
   const long long s = trans ? m : n;
-  if (emulation_on(h) && s <= EMU_K) {   // one exact int32 pass over K = s
-    const geninv_status es = trans ? apply_emulated_t(h, G, m, n, ld, Gp, ldp, st)
-                                   : apply_emulated(h, G, m, n, ld, Gp, ldp, st);
+  if (emulation_on(h) && s <= 16384) {
+    const geninv_status es = apply_emulated(h, G, m, n, ld, trans, Gp, ldp, st);
     if (es != GENINV_ERANGE) return es;   // out of the emulation's range: the native product below
   }
   GemmOp op;

@@ -131,3 +131,19 @@ def test_emulated_nonfinite_and_zero(H):
         assert info.rank == 0 and not Gp.any()
     finally:
         H.set_emulation(0)
+
+
+@pytest.mark.parametrize("m,n,seed", [(6200, 4500, 10700), (4500, 6200, 10701)])   # seeds in Q (oracle)
+def test_emulated_two_k_passes(H, m, n, seed):
+    """s = 4500 > 4096: a7 over two exact int32 K passes with their own exponents, the Gram in
+    K-chunks (both branches)."""
+    G = I.low_rank(seed, m, n, 4300, device="cuda")
+    H.set_emulation(1)
+    Gp, info = H.geninv_d(G)
+    H.set_emulation(0)
+    Gh = G.cpu().numpy()
+    R = O.geninv(Gh)
+    assert R.in_Q()
+    assert info.rank == R.rank == 4300
+    assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
+    assert max(penrose(Gh, Gp.cpu().numpy())) <= 1e-10
