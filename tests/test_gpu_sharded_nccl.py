@@ -1,6 +1,7 @@
 """geninv_sharded_d through a real NCCL communicator (`-m gpu`).  On the single GPU of the test box
 the process group has one rank, so the all-reduce is the identity: the call must reproduce
-geninv_d bit for bit, in both sharding modes (rows of a tall G, columns of a wide G).  The
+geninv_d bit for bit, in both sharding modes (rows of a tall G, columns of a wide G), on the DMMA
+path and with the Gram / a7 emulated on the INT8 tensor cores.  The
 multi-rank orchestration is covered on CPU by tests/test_sharded_gloo.py."""
 import os
 import socket
@@ -39,12 +40,15 @@ def H():
     return Handle(0)
 
 
-@pytest.mark.parametrize("m,n,r,trans", [(3000, 400, 300, 0), (400, 3000, 300, 1)])
-def test_sharded_single_rank_equals_geninv(H, comm, m, n, r, trans):
+@pytest.mark.parametrize("emulate", [0, 1], ids=["dmma", "int8_emulated"])
+@pytest.mark.parametrize("m,n,r,trans", [(3000, 400, 300, 0), (400, 3000, 300, 1), (9000, 3200, 3000, 0)])
+def test_sharded_single_rank_equals_geninv(H, comm, m, n, r, trans, emulate):
     G = I.low_rank(m + 11 * n, m, n, r, device="cuda")
+    H.set_emulation(emulate)
     whole, info = H.geninv_d(G)
     Gp = torch.empty(n, m, dtype=torch.float64, device="cuda")
     _, sinfo = H.geninv_sharded_d(comm, G, trans, Gp)
+    H.set_emulation(0)
     assert sinfo.rank == info.rank == r
     R = O.geninv(G.cpu().numpy())
     if R.in_Q():
