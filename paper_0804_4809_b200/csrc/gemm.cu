@@ -196,6 +196,14 @@ static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
   return bs;
 }
 
+int upd_tile_bm() {
+  static const int bm = [] {
+    const char *e = getenv("GENINV_UPD_TILE_BM");   // measurements: 128 = the earlier 128 x 32 tile
+    return (e && atoi(e) == 128) ? 128 : 256;
+  }();
+  return bm;
+}
+
 cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
   if (op.M <= 0 || op.N <= 0) return cudaSuccess;
   if (op.lower && op.M != op.N) return cudaErrorInvalidValue;
@@ -208,6 +216,9 @@ cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
   a.k_lo_mode = op.k_lo_mode; a.k_hi_mode = op.k_hi_mode; a.k_lo_dev = op.k_lo_dev;
   a.lower = op.lower; a.mirror = op.mirror; a.splits = op.splits < 1 ? 1 : op.splits;
   if (op.tile == TILE_128x32) {
+    // the panel update (K-major L both sides): 256 x 32 tiles, 8 warps = two per SM sub-partition
+    // (the 128 x 32 tile keeps one warp per sub-partition with the DMMA pipe ~47 % busy)
+    if (op.a_kmajor && op.b_kmajor && upd_tile_bm() == 256) return launch<256, 32, 32, 32, 6, true, true>(op, a, st);
     if (op.a_kmajor && op.b_kmajor) return launch<128, 32, 32, 32, 6, true, true>(op, a, st);
     if (op.a_kmajor && !op.b_kmajor) return launch<128, 32, 32, 32, 6, true, false>(op, a, st);
     if (!op.a_kmajor && op.b_kmajor) return launch<128, 32, 32, 32, 6, false, true>(op, a, st);

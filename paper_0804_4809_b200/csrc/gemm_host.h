@@ -12,7 +12,7 @@ struct Mat {               // row-major device matrix (or batch of equally-shape
   long long bstride = 0;   // elements between batch items
 };
 
-enum Tile { TILE_128x128 = 0, TILE_128x32 = 1 };
+enum Tile { TILE_128x128 = 0, TILE_128x32 = 1 };   // TILE_128x32: N = 32 panel updates (256 x 32 when both operands are K-major, see upd_tile_bm)
 
 struct GemmOp {
   Mat A;  bool a_kmajor = true;  int a_mn0 = 0, a_k0 = 0;
@@ -31,6 +31,7 @@ struct GemmOp {
 };
 
 // Enqueue one GEMM on `st`.  Returns cudaSuccess or the launch / encode error.
+int upd_tile_bm();   // rows of the panel update's tiles (TILE_128x32 with K-major operands): 256, or 128
 cudaError_t gemm(const GemmOp &op, cudaStream_t st);
 
 // Sum split-K partial slices in a fixed order:  out = C0 + alpha * sum_z P[z]

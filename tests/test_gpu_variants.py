@@ -46,12 +46,13 @@ VARIANTS = {
     "one_stream": {"GENINV_ONE_UPD_STREAM": "1"},
     "no_graph": {"GENINV_NO_GRAPH": "1"},
     "no_chain_split": {"GENINV_CHAIN_SPLIT": "0"},
+    "upd_tile_128": {"GENINV_UPD_TILE_BM": "128"},
 }
 
 
 def run_variant(tmp_path, name, env_extra):
     env = dict(os.environ)
-    for k in ("GENINV_LOOKAHEAD", "GENINV_ONE_UPD_STREAM", "GENINV_NO_GRAPH", "GENINV_CHAIN_SPLIT"):
+    for k in ("GENINV_LOOKAHEAD", "GENINV_ONE_UPD_STREAM", "GENINV_NO_GRAPH", "GENINV_CHAIN_SPLIT", "GENINV_UPD_TILE_BM"):
         env.pop(k, None)
     env.update(env_extra)
     prefix = str(tmp_path / name)

@@ -43,3 +43,7 @@ med = np.median(d[2:-1], axis=0)
 print(f"s={n}: {np_} panels; median us per phase (panels >= 2): " +
       ", ".join(f"{a} {b:.2f}" for a, b in zip(names, med)) + f"; gap to next {np.median(gap):.2f}")
 print(f"  span of the whole factorisation: {(end[-1] - t[0, 0]) / 1e3:.0f} us")
+kern = d[:, 6]
+print(f"  sum of kernel times {kern.sum():.0f} us, sum of gaps {gap.sum():.0f} us; gap percentiles 50/90/99: "
+      + " / ".join(f"{np.percentile(gap, q):.2f}" for q in (50, 90, 99))
+      + "; largest gaps (panel: us): " + ", ".join(f"{i + 1}: {gap[i]:.1f}" for i in np.argsort(gap)[::-1][:8]))
