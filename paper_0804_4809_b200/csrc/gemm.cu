@@ -157,6 +157,9 @@ static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
   if (op.lower) {
     for (int bi = 0; bi < mt; ++bi)
       for (int bj = 0; bj <= bi; ++bj) len.push_back(tile_len(bi, bj));
+  } else if (op.k_hi_mode) {   // the kernel's LPT order (M-tiles descending, N fastest)
+    for (int tm = mt - 1; tm >= 0; --tm)
+      for (int tn = 0; tn < nt; ++tn) len.push_back(tile_len(tm, tn));
   } else {
     for (int band = 0; band * mband < mt; ++band) {
       const int mb = std::min(mband, mt - band * mband);

@@ -82,6 +82,11 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
       while (bi * (bi + 1) / 2 > t) --bi;
       tm = bi;
       tn = t - bi * (bi + 1) / 2;
+    } else if (p.k_hi_mode) {
+      // the k-range grows with the M-tile (A trapezoidal: K = L M, TRTRI's C22 products): longest
+      // tiles first (LPT order, N fastest), so the last partial wave holds the short ones
+      tm = p.mtiles - 1 - t / p.ntiles;
+      tn = t - (t / p.ntiles) * p.ntiles;
     } else {
       // banded raster: M fastest inside a band of mband M-tiles, then N, then the next band, so the
       // A rows of one band (sized on the host to fit the L2) are re-read from L2, not HBM.
