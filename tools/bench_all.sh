@@ -9,3 +9,4 @@ done
 for w in C4 C3T C3 C2; do
   timeout 900 python bench.py --workload $w --emulate > $out/r01_bench_$(echo $w | tr A-Z a-z)_emulated_n1.json 2> $out/${w}_emu.err
 done
+timeout 900 python bench.py --impl reference > $out/r01_bench_reference_n1.json 2> $out/reference.err
