@@ -994,10 +994,16 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
     h->gdev_bytes = gbytes;
   }
   GI_TRYS(ensure_ws(h, s));
-  // ---- H2D in chunks of ~1/16 of G (32 .. 256 MB), the Gram of each chunk accumulated as soon as it
+  // ---- H2D in chunks of ~1/8 of G (64 .. 256 MB; C3 / C3T e2e: 32 MB chunks 38.9 ms, 64 MB 36.5,
+  //      128 MB 37.4), the Gram of each chunk accumulated as soon as it
   //      lands: N branch row chunks (A = sum_c G_c' G_c), T branch column chunks (A = sum_c G_c G_c'),
   //      summed in chunk order (deterministic)
-  const long long target = std::min<long long>(256LL << 20, std::max<long long>(32LL << 20, (long long)gbytes / 16));
+  static const long long chunk_mb = [] {   // tuning override of the chunk size (MB)
+    const char *e = getenv("GENINV_HOST_CHUNK_MB");
+    return e ? atoll(e) : 0LL;
+  }();
+  const long long target = chunk_mb > 0 ? (chunk_mb << 20)
+                                        : std::min<long long>(256LL << 20, std::max<long long>(64LL << 20, (long long)gbytes / 8));
   if (!tr) {
     const long long rows_per = std::max<long long>(1, target / (ldg * 8));
     for (long long r0 = 0; r0 < m; r0 += rows_per) {

@@ -284,10 +284,11 @@ def test_batched_deterministic(H):
         assert torch.equal(Gp, ref)
 
 
-@pytest.mark.parametrize("m,n,r", [(40000, 300, 250), (300, 40000, 250)])
+@pytest.mark.parametrize("m,n,r", [(90000, 300, 250), (300, 90000, 250)])
 def test_host_buffers_chunked(H, m, n, r):
-    # ~96 MB inputs: the host path copies and accumulates the Gram in 3 chunks (rows for m >= n,
-    # columns for m < n) and streams G+ back in chunks; same result as the device path
+    # ~216 MB inputs: the host path copies and accumulates the Gram in 4 chunks of 64 MB (rows for
+    # m >= n, columns for m < n; the last one partial) and streams G+ back in chunks; same result
+    # as the device path
     G = I.low_rank(m + 2 * n, m, n, r).numpy()
     dev_gp, dev_info = run(H, G)
     Gh = torch.as_tensor(G).pin_memory()
