@@ -42,6 +42,7 @@ print(json.dumps(out))
 VARIANTS = {
     "default": {},
     "depth1": {"GENINV_LOOKAHEAD": "1"},
+    "depth2": {"GENINV_LOOKAHEAD": "2"},
     "depth3": {"GENINV_LOOKAHEAD": "3"},
     "one_stream": {"GENINV_ONE_UPD_STREAM": "1"},
     "no_graph": {"GENINV_NO_GRAPH": "1"},
