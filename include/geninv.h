@@ -30,8 +30,13 @@
  *     that return a host-side rank / info synchronise that stream.
  *   - Errors are status codes; nothing throws across the ABI.  A handle is
  *     not thread-safe; separate handles are independent.
- *   - Alignment: the TMA path needs 16-byte-aligned base pointers and even
- *     leading dimensions; other inputs are rejected with GENINV_EALIGN.
+ *   - Alignment: any leading dimension ld >= n and any (8-byte aligned)
+ *     base pointer is accepted.  The tensor-core path reads G, F and L with
+ *     TMA, which needs 16-byte-aligned bases and even leading dimensions: an
+ *     operand without them is first copied (stream-ordered, device to device)
+ *     into a handle-owned aligned buffer -- one extra m x n doubles of device
+ *     memory and one copy; aligned operands are read in place.  Outputs
+ *     (G+, W, M, X) are written with plain stores: any ldp works.
  */
 #ifndef GENINV_H_
 #define GENINV_H_
@@ -55,7 +60,7 @@ typedef enum {
   GENINV_ENOTSPD = 3,     /* a5: a pivot <= 0 in the Cholesky of L'L (reading R8) */
   GENINV_ECUDA = 4,       /* CUDA runtime / launch error */
   GENINV_ENOMEM = 5,      /* device allocation failed */
-  GENINV_EALIGN = 6,      /* pointer not 16-byte aligned or odd leading dimension */
+  GENINV_EALIGN = 6,      /* reserved: no longer returned (unaligned operands are staged, see above) */
   GENINV_ESTATE = 7,      /* geninv_apply_d before geninv_from_gram_d, or shape mismatch */
   GENINV_ENCCL = 8,       /* geninv_sharded_d: libnccl.so.2 not loadable or ncclAllReduce failed */
   GENINV_ERANGE = 9       /* an accepted pivot below 2^-1022 (subnormal, ~2.2e-308): |G| is too
@@ -108,7 +113,7 @@ GENINV_API const char *geninv_strerror(geninv_status st);
  * rank (host, may be NULL) receives r; info (host, may be NULL) diagnostics.
  * Zero G -> rank 0 and G+ = 0 (reading R2).  Synchronises the stream.
  * Small matrices (min(m, n) <= 64, max(m, n) <= 128) run the whole path in one
- * CTA (the batched kernel, a9; any alignment and leading dimension); that path does not keep X in the handle
+ * CTA (the batched kernel, a9; G read in place at any alignment); that path does not keep X in the handle
  * (geninv_copy_x then returns GENINV_ESTATE).  For low rank, where
  * 4 r s l < s (s + 1) r + 2 s^2 l (s = min(m, n), l = max(m, n)), geninv_d skips
  * X and evaluates G+ = K (K' G') (m >= n) or (G' K) K' (m < n) with K = L M,
@@ -149,8 +154,8 @@ GENINV_API geninv_status geninv_batched_d(geninv_handle h, const double *G, int6
  * W = G+ F, the paper's use of G+ for RBF synaptic weights (P:22, P:32-34 with
  * the "W = G+ W" typo read as W = G+ F, reading R10), without forming
  * G+: N branch (m >= n) W = X (G' F), T branch (m < n) W = G' (X F), with
- * X = L M M L' from steps a1-a6.  G: m x n (ld >= n), F: m x k (ldf >= k, even,
- * 16-byte aligned), W: n x k (ldw >= k), all device, row-major; W is written.
+ * X = L M M L' from steps a1-a6.  G: m x n (ld >= n), F: m x k (ldf >= k),
+ * W: n x k (ldw >= k), all device, row-major; W is written.
  * rank / info as for geninv_d.  Synchronises.  The s x k intermediate lives
  * in the handle's workspace. */
 GENINV_API geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld,
@@ -168,6 +173,11 @@ GENINV_API geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_
  * same r and X); the output needs no further communication.  nccl_comm is an
  * ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()); NCCL is resolved at
  * run time from the already-loaded libnccl.so.2 (GENINV_ENCCL if absent).
+ * Collective call: every rank of the communicator must call it.  Before the
+ * all-reduce of A the ranks exchange (status, s) in one small MAX all-reduce,
+ * so a local failure on any rank (bad arguments, ENOMEM, a CUDA error in its
+ * Gram) or s differing between ranks returns that status (EINVAL for the shape)
+ * on EVERY rank instead of blocking the others.
  * Synchronises; rank / info as for geninv_d. */
 GENINV_API geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G_local, int64_t m_local,
                                int64_t n, int64_t ld, int32_t trans, double *Gp_local, int64_t ldp, int64_t *rank,

@@ -228,13 +228,45 @@ def apply(X: np.ndarray, G: np.ndarray) -> np.ndarray:
     return X @ G.T
 
 
+def full_rank_cholesky_batched(A, tol):
+    """P:118-133 for a stack of independent Gram matrices A (batch, s, s) with per-matrix tol (batch,).
+
+    The loop is that of full_rank_cholesky, vectorised over the independent batch index only;
+    columns not yet accepted are zero, so the correction sums over all s columns add exact zeros.
+    Returns (L (batch, s, s) with the kept columns first, r int64[batch], min_acc, max_drop,
+    min_pivot) -- min_acc = min accepted c_k (+inf if none), max_drop = max |dropped c_k| (0 if
+    none), min_pivot = min over all c_k (SURVEY §8(c4) margins).
+    """
+    A = np.asarray(A, dtype=np.float64)
+    tol = np.asarray(tol, dtype=np.float64)
+    nb, s, _ = A.shape
+    L = np.zeros((nb, s, s))
+    r = np.zeros(nb, dtype=np.int64)
+    min_acc = np.full(nb, np.inf)
+    max_drop = np.zeros(nb)
+    min_piv = np.full(nb, np.inf)
+    ar = np.arange(nb)
+    for k in range(s):
+        c = A[:, k:, k] - np.matmul(L[:, k:, :], L[:, k, :, None])[..., 0]    # P:122
+        ok = c[:, 0] > tol                                                    # P:124, strict (R3)
+        d = np.sqrt(np.where(ok, c[:, 0], 1.0))                               # P:125
+        idx = ar[ok]
+        L[idx, k, r[idx]] = d[idx]
+        if k < s - 1:
+            L[idx, k + 1:, r[idx]] = c[idx, 1:] / d[idx, None]                # P:127
+        min_acc[idx] = np.minimum(min_acc[idx], c[idx, 0])
+        nd = ar[~ok]
+        max_drop[nd] = np.maximum(max_drop[nd], np.abs(c[nd, 0]))
+        min_piv = np.minimum(min_piv, c[:, 0])
+        r[idx] += 1
+    return L, r, min_acc, max_drop, min_piv
+
+
 def geninv_batched(Gb, tol_rel: float = TOL_REL):
     """geninv applied independently to each matrix of a (batch, m, n) stack.
 
-    The Cholesky loop of P:118-133 runs for all matrices at once (vectorised
-    over the independent batch index only; within a matrix the order of
-    operations is that of full_rank_cholesky).  Columns not yet accepted are
-    zero, so the correction sums over all s columns add exact zeros only.
+    Gram and tolerance per matrix, the Cholesky loop of P:118-133
+    through full_rank_cholesky_batched, then P:135-139 per matrix.
     Returns (Gp (batch, n, m), rank int64[batch], mu_acc, mu_drop).
     """
     Gb = np.asarray(Gb, dtype=np.float64)
@@ -243,27 +275,10 @@ def geninv_batched(Gb, tol_rel: float = TOL_REL):
     nb, m, n = Gb.shape
     transposed = m < n
     A = Gb @ np.swapaxes(Gb, 1, 2) if transposed else np.swapaxes(Gb, 1, 2) @ Gb
-    s = A.shape[1]
     dA = np.diagonal(A, axis1=1, axis2=2)
     pos = np.where(dA > 0, dA, np.inf).min(axis=1)
     tol = np.where(np.isfinite(pos), pos * tol_rel, 0.0)
-    L = np.zeros((nb, s, s))
-    r = np.zeros(nb, dtype=np.int64)
-    min_acc = np.full(nb, np.inf)
-    max_drop = np.zeros(nb)
-    ar = np.arange(nb)
-    for k in range(s):
-        c = A[:, k:, k] - np.matmul(L[:, k:, :], L[:, k, :, None])[..., 0]
-        ok = c[:, 0] > tol
-        d = np.sqrt(np.where(ok, c[:, 0], 1.0))
-        idx = ar[ok]
-        L[idx, k, r[idx]] = d[idx]
-        if k < s - 1:
-            L[idx, k + 1:, r[idx]] = c[idx, 1:] / d[idx, None]
-        min_acc[idx] = np.minimum(min_acc[idx], c[idx, 0])
-        nd = ar[~ok]
-        max_drop[nd] = np.maximum(max_drop[nd], np.abs(c[nd, 0]))
-        r[idx] += 1
+    L, r, min_acc, max_drop, _ = full_rank_cholesky_batched(A, tol)
     Gp = np.zeros((nb, n, m))
     for rv in np.unique(r):
         if rv == 0:

@@ -223,10 +223,6 @@ class Handle:
         """Minimum-norm least-squares W = G+ F (G: m x n, F: m x k) -> (W (n x k), Info)."""
         m, n = G.shape
         k = F.shape[1]
-        if F.stride(0) % 2 or F.stride(1) != 1 or F.data_ptr() % 16:   # the TMA view needs an even, aligned ld
-            Fp = torch.zeros(m, (k + 1) // 2 * 2, dtype=torch.float64, device=F.device)
-            Fp[:, :k] = F
-            F = Fp[:, :k]
         if W is None:
             W = torch.empty(n, k, dtype=torch.float64, device=G.device)
         info = _Info()

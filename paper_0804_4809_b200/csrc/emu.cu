@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "emu.h"
+#include "gemm_host.h"
 
 namespace gi {
 
@@ -412,16 +413,7 @@ cudaError_t slice_map(CUtensorMap *m, const int8_t *p, int rows, int Kp, int S, 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-int num_sms_emu() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
+int num_sms_emu() { return num_sms(); }   // per device (gemm.cu)
 
 }  // namespace
 
@@ -453,12 +445,7 @@ cudaError_t emu_gemm_nt(const int8_t *As, const int *ea, int M, const int8_t *Bs
   cudaError_t e = slice_map(&ta, As, M, Kp, S, EBM);
   if (e != cudaSuccess) return e;
   if ((e = slice_map(&tb, Bs, N, Kp, S, EBN)) != cudaSuccess) return e;
-  static bool attr = false;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(emu_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ESMEM)) != cudaSuccess)
-      return e;
-    attr = true;
-  }
+  if ((e = smem_optin((const void *)emu_gemm_kernel, ESMEM)) != cudaSuccess) return e;
   emu_gemm_kernel<<<emu_ctas(M, N, lower), ENT, ESMEM, st>>>(ta, tb, ea, eb, C, ldc, M, N, Kp, S, T, scratch,
                                                               lower, accumulate);
   return cudaGetLastError();

@@ -9,6 +9,8 @@
 #include <queue>
 #include <vector>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "gemm.cuh"
 #include "gemm_host.h"
@@ -31,14 +33,30 @@ static cudaError_t get_encode() {
 }
 
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  constexpr int MAXDEV = 64;
+  static int sms[MAXDEV] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= MAXDEV) dev = 0;
+  if (!sms[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
   }
-  return sms;
+  return sms[dev];
+}
+
+cudaError_t smem_optin(const void *fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({fn, dev});
+  return e;
 }
 
 // 3-D map {cols (contiguous), rows, batch}; box {16, box_rows, 1}; 128B swizzle;
@@ -80,17 +98,12 @@ static cudaError_t make_map_mn4d(CUtensorMap *map, const Mat &m, int strips) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int BM, int BN, int WM, int WN, int ST, bool AK, bool BK_>
+template <int BM, int BN, int WM, int WN, int ST, bool AK, bool BK_, bool CHUNK = false>
 static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM, WN, ST, AK, BK_>;
-  auto kern = dgemm_tc<BM, BN, WM, WN, ST, AK, BK_>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  cudaError_t e;
+  auto kern = dgemm_tc<BM, BN, WM, WN, ST, AK, BK_, CHUNK>;
+  cudaError_t e = smem_optin((const void *)kern, Cfg::SMEM);
+  if (e != cudaSuccess) return e;
   a.a_mn4d = !AK && (op.A.cols % 16 == 0) && (op.a_mn0 % 16 == 0);
   a.b_mn4d = !BK_ && (op.B.cols % 16 == 0) && (op.b_mn0 % 16 == 0);
   e = a.a_mn4d ? make_map_mn4d(&a.tmA, op.A, BM / 16) : make_map(&a.tmA, op.A, AK ? BM : 16);
@@ -218,6 +231,13 @@ cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
   a.alpha = op.alpha; a.M = op.M; a.N = op.N; a.K = op.K; a.K_dev = op.K_dev;
   a.k_lo_mode = op.k_lo_mode; a.k_hi_mode = op.k_hi_mode; a.k_lo_dev = op.k_lo_dev;
   a.lower = op.lower; a.mirror = op.mirror; a.splits = op.splits < 1 ? 1 : op.splits;
+  a.kchunk = op.kchunk;
+  if (op.kchunk > 0) {   // the Gram (a1): both operands K-major (T branch) or both MN-major (N branch)
+    if (op.alpha != 1.0 || op.C0 || op.mirror || op.tile != TILE_128x128) return cudaErrorInvalidValue;
+    if (op.a_kmajor && op.b_kmajor) return launch<128, 128, 64, 32, 6, true, true, true>(op, a, st);
+    if (!op.a_kmajor && !op.b_kmajor) return launch<128, 128, 64, 32, 6, false, false, true>(op, a, st);
+    return cudaErrorInvalidValue;
+  }
   if (op.tile == TILE_128x32) {
     // the panel update (K-major L both sides): 256 x 32 tiles, 8 warps = two per SM sub-partition
     // (the 128 x 32 tile keeps one warp per sub-partition with the DMMA pipe ~47 % busy)
@@ -242,14 +262,21 @@ __global__ void splitk_reduce_kernel(const double *__restrict__ P, long long sst
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx / N), j = (int)(idx % N);
     if (lower && j > i) continue;
-    double v[16];   // every slice in flight at once (splits <= 16 here; more: the tail loop), summed in order
+    // slices summed pairwise (a fixed tree: deterministic, and the rounding error grows like log2 of the
+    // slice count instead of its square root): groups of 16 in flight at once, then the group sums
+    double gs[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int z0 = 0, gi = 0; z0 < splits; z0 += 16, ++gi) {
+      double v[16];
 #pragma unroll
-    for (int z = 0; z < 16; ++z) v[z] = z < splits ? P[z * sstride + (long long)i * ldp + j] : 0.0;
-    double s = 0.0;
+      for (int z = 0; z < 16; ++z) v[z] = z0 + z < splits ? P[(z0 + z) * sstride + (long long)i * ldp + j] : 0.0;
 #pragma unroll
-    for (int z = 0; z < 16; ++z)
-      if (z < splits) s += v[z];
-    for (int z = 16; z < splits; ++z) s += P[z * sstride + (long long)i * ldp + j];
+      for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+        for (int z = 0; z < 16; z += 2 * w) v[z] += v[z + w];
+      if (gi < 4) gs[gi] = v[0];
+      else gs[3] += v[0];   // beyond 64 slices (not used by the library's split counts)
+    }
+    const double s = (gs[0] + gs[1]) + (gs[2] + gs[3]);
     double o = alpha * s;
     if (C0) o += C0[(long long)i * ldc0 + j];
     out[(long long)i * ldo + j] = o;

@@ -41,6 +41,8 @@ struct GemmArgs {
   int mirror;               // 1 (with lower): also store C[n][m]; diagonal tiles store m >= n mirrored
   int splits;               // split-K count
   int a_mn4d, b_mn4d;       // MN-major operand mapped as a 4-D {16, k, mn/16, batch} view: one TMA op per tile
+  int kchunk;               // CHUNK instances: k-slabs per register accumulation; each chunk's sum is added
+                            //   into the CTA's output tile in memory (two-level accumulation, see below)
 };
 
 // row permutation inside an 8-row fragment: makes the LDS.128 fragment loads
@@ -59,7 +61,45 @@ struct GemmCfg {
   static_assert(WM % 16 == 0 && WN % 16 == 0, "warp tile must be a multiple of 16");
 };
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool A_K, bool B_K>
+// Output tile (tm, tn) of CTA t: lower-triangle enumeration, LPT order for growing k-ranges, or the
+// banded raster of the general case.
+GI_DEV void tile_of(const GemmArgs &p, int t, int &tm, int &tn) {
+  if (p.lower) {
+    // t -> (bi, bj), bj <= bi, row-major over the lower triangle
+    int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    while (bi * (bi + 1) / 2 > t) --bi;
+    tm = bi;
+    tn = t - bi * (bi + 1) / 2;
+  } else if (p.k_hi_mode) {
+    // the k-range grows with the M-tile (A trapezoidal: K = L M, TRTRI's C22 products): longest
+    // tiles first (LPT order, N fastest), so the last partial wave holds the short ones
+    tm = p.mtiles - 1 - t / p.ntiles;
+    tn = t - (t / p.ntiles) * p.ntiles;
+  } else {
+    // banded raster: M fastest inside a band of mband M-tiles, then N, then the next band, so the
+    // A rows of one band (sized on the host to fit the L2) are re-read from L2, not HBM.
+    const int band_tiles = p.mband * p.ntiles;
+    const int band = t / band_tiles;
+    const int rem = t - band * band_tiles;
+    const int mb = min(p.mband, p.mtiles - band * p.mband);
+    tm = band * p.mband + rem % mb;
+    tn = rem / mb;
+  }
+}
+
+// Special registers read without CSE (the CHUNK flush re-derives its coordinates instead of keeping
+// them live across the main loop).
+GI_DEV int fresh_ctaid_x() { int v; asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(v)); return v; }
+GI_DEV int fresh_ctaid_y() { int v; asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(v)); return v; }
+GI_DEV int fresh_tid_x() { int v; asm volatile("mov.u32 %0, %%tid.x;" : "=r"(v)); return v; }
+
+// CHUNK (the Gram, a1): the k-range of a CTA is accumulated in register chunks of p.kchunk slabs; after
+// each chunk the warp adds its fragment sums into the output tile in memory (the first chunk stores) and
+// restarts from zero.  A 2^21-row Gram then sums ~8k-row partials instead of ~57k-row sequential chains
+// (rounding error of a sequential sum grows like sqrt(length)); every element is owned by one thread, so
+// the read-back needs no synchronisation, and the order is fixed (deterministic).
+template <int BM, int BN, int WM, int WN, int STAGES, bool A_K, bool B_K, bool CHUNK = false>
 __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THREADS, 1)
     dgemm_tc(const __grid_constant__ GemmArgs p) {
   using Cfg = GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>;
@@ -73,31 +113,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
 
   // ---- tile coordinates
   int tm, tn;
-  {
-    int t = blockIdx.x;
-    if (p.lower) {
-      // t -> (bi, bj), bj <= bi, row-major over the lower triangle
-      int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-      while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-      while (bi * (bi + 1) / 2 > t) --bi;
-      tm = bi;
-      tn = t - bi * (bi + 1) / 2;
-    } else if (p.k_hi_mode) {
-      // the k-range grows with the M-tile (A trapezoidal: K = L M, TRTRI's C22 products): longest
-      // tiles first (LPT order, N fastest), so the last partial wave holds the short ones
-      tm = p.mtiles - 1 - t / p.ntiles;
-      tn = t - (t / p.ntiles) * p.ntiles;
-    } else {
-      // banded raster: M fastest inside a band of mband M-tiles, then N, then the next band, so the
-      // A rows of one band (sized on the host to fit the L2) are re-read from L2, not HBM.
-      const int band_tiles = p.mband * p.ntiles;
-      const int band = t / band_tiles;
-      const int rem = t - band * band_tiles;
-      const int mb = min(p.mband, p.mtiles - band * p.mband);
-      tm = band * p.mband + rem % mb;
-      tn = rem / mb;
-    }
-  }
+  tile_of(p, blockIdx.x, tm, tn);
   const int split = blockIdx.y, bz = blockIdx.z;
   const int m0 = tm * BM, n0 = tn * BN;
   const int K = p.K_dev ? *p.K_dev : p.K;
@@ -178,6 +194,53 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
   for (int i = 0; i < FM; ++i)
 #pragma unroll
     for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // registers -> the output tile; add = 1: add to what this thread stored before (CHUNK only)
+  auto chunk_out = [&](bool add, int tm, int tn, int split, int wm, int wn, int g, int t, int pg) {
+    const int m0 = tm * BM, n0 = tn * BN;
+    const bool diag_tile = p.lower && (tm == tn);
+    double *Cb = p.C + (long long)bz * p.c_bstride + (p.splits > 1 ? (long long)split * p.split_stride : 0);
+    const double *C0b = (p.C0 && p.splits == 1) ? p.C0 + (long long)bz * p.c0_bstride : nullptr;
+    const double alpha = (p.splits > 1) ? 1.0 : p.alpha;
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      int m;
+      if (A_K) m = m0 + wm * WM + i * 8 + pg;
+      else m = m0 + wm * WM + 16 * (i >> 1) + 2 * g + (i & 1);
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          int n;
+          if (B_K) n = n0 + wn * WN + j * 8 + t + 4 * v;
+          else n = n0 + wn * WN + 16 * (j >> 1) + 4 * t + 2 * v + (j & 1);
+          if (n >= p.N) continue;
+          if (p.lower && diag_tile && n > m) continue;  // diagonal tiles: keep m >= n
+          double *cp = Cb + (long long)m * p.ldc + n;
+          if (CHUNK) {   // Gram: alpha = 1, no addend, no mirror
+            *cp = add ? *cp + acc[i][j][v] : acc[i][j][v];
+          } else {
+            double val = alpha * acc[i][j][v];
+            if (C0b) val += C0b[(long long)m * p.ldc0 + n];
+            *cp = val;
+            if (p.mirror && n != m) Cb[(long long)n * p.ldc + m] = val;
+          }
+        }
+      }
+    }
+  };
+
+  // CHUNK: coordinates re-derived from fresh special-register reads (nothing of the epilogue stays live
+  // across the main loop: the two-operand K-major instance would otherwise spill)
+  auto flush = [&](bool add) {
+    int ftm, ftn;
+    tile_of(p, fresh_ctaid_x(), ftm, ftn);
+    const int tid = fresh_tid_x();
+    const int fg = (tid & 31) >> 2;
+    chunk_out(add, ftm, ftn, fresh_ctaid_y(), (tid >> 5) % Cfg::NWM, (tid >> 5) / Cfg::NWM, fg, tid & 3,
+              frag_perm(fg));
+  };
 
   const uint32_t sbase = smem_u32(smem);
   for (int it = 0; it < nslab; ++it) {
@@ -261,35 +324,18 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WM, WN, STAGES, A_K, B_K>::THR
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+    if (CHUNK && (it + 1) % p.kchunk == 0 && it + 1 < nslab) {
+      flush(it + 1 > p.kchunk);
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
   }
 
   // ================= epilogue (registers -> global) =================
-  const bool diag_tile = p.lower && (tm == tn);
-  double *Cb = p.C + (long long)bz * p.c_bstride + (p.splits > 1 ? (long long)split * p.split_stride : 0);
-  const double *C0b = (p.C0 && p.splits == 1) ? p.C0 + (long long)bz * p.c0_bstride : nullptr;
-  const double alpha = (p.splits > 1) ? 1.0 : p.alpha;
-#pragma unroll
-  for (int i = 0; i < FM; ++i) {
-    int m;
-    if (A_K) m = m0 + wm * WM + i * 8 + pg;
-    else m = m0 + wm * WM + 16 * (i >> 1) + 2 * g + (i & 1);
-    if (m >= p.M) continue;
-#pragma unroll
-    for (int j = 0; j < FN; ++j) {
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        int n;
-        if (B_K) n = n0 + wn * WN + j * 8 + t + 4 * v;
-        else n = n0 + wn * WN + 16 * (j >> 1) + 4 * t + 2 * v + (j & 1);
-        if (n >= p.N) continue;
-        if (p.lower && diag_tile && n > m) continue;  // diagonal tiles: keep m >= n
-        double val = alpha * acc[i][j][v];
-        if (C0b) val += C0b[(long long)m * p.ldc0 + n];
-        Cb[(long long)m * p.ldc + n] = val;
-        if (p.mirror && n != m) Cb[(long long)n * p.ldc + m] = val;
-      }
-    }
-  }
+  if (CHUNK) flush(nslab > p.kchunk);
+  else chunk_out(false, tm, tn, split, wm, wn, g, t, pg);
 }
 
 }  // namespace gi

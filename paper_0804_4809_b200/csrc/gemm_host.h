@@ -27,6 +27,8 @@ struct GemmOp {
   int batch = 1;
   bool lower = false, mirror = false;
   int splits = 1; long long split_stride = 0;
+  int kchunk = 0;                // > 0: two-level accumulation in chunks of kchunk k-slabs (alpha 1, no C0 /
+                                 //   mirror; 128 x 128 tiles) -- the Gram's accuracy over millions of rows
   Tile tile = TILE_128x128;
 };
 
@@ -41,7 +43,11 @@ cudaError_t splitk_reduce(const double *P, long long split_stride, int splits, l
                           long long ldo, const double *C0, long long ldc0, double alpha, int M, int N, bool lower,
                           cudaStream_t st, bool mirror = false);
 
-int num_sms();
+int num_sms();   // SM count of the current device (cached per device)
+
+// Opt `fn` in to `bytes` of dynamic shared memory on the CURRENT device (the attribute is per device /
+// context: done once per (kernel, device), thread-safe).
+cudaError_t smem_optin(const void *fn, int bytes);
 
 // Split-K count for a 128 x 128 launch from a schedule simulation (see gemm.cu); 1 = no split.
 int balanced_splits(const GemmOp &op, int max_splits, int sms);

@@ -54,6 +54,10 @@ struct geninv_handle_s {
   // least-squares solve (f1): the s x k intermediate G'F or X F
   double *T1 = nullptr;
   size_t t1_bytes = 0;
+  // aligned copies of caller operands the TMA path cannot read in place (stage_operand)
+  double *stage[2] = {nullptr, nullptr};
+  double *coll = nullptr;   // geninv_sharded_d: the small pre-check all-reduce buffer
+  size_t stage_bytes[2] = {0, 0};
   // a7 emulated on the INT8 tensor cores (geninv_set_emulation): slices of X and of a chunk of G
   int emulate = -1;        // -1: not set (GENINV_EMULATE decides), 0 native DMMA, 1 emulated
   int8_t *emu_x = nullptr, *emu_g = nullptr;
@@ -230,6 +234,17 @@ geninv_status gram_emulated(geninv_handle h, const double *G, long long m, long 
   return flag ? GENINV_ERANGE : GENINV_OK;
 }
 
+// Rows of G per register-accumulated partial sum of the DMMA Gram (GENINV_GRAM_CHUNK_ROWS; 0 = one
+// sequential sum per CTA).  8192: C4's 2^21-row sums become 8k-row partials added in a fixed order.
+int gram_chunk_rows() {
+  static const int rows = [] {
+    const char *e = getenv("GENINV_GRAM_CHUNK_ROWS");
+    const int v = e ? atoi(e) : 8192;
+    return v <= 0 ? 0 : std::max(16, v / 16 * 16);
+  }();
+  return rows;
+}
+
 // a1: A (s x s, lower) = G'G (trans == 0) or GG' (trans == 1).
 geninv_status gram(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *A,
                    long long lda, const double *accumulate = nullptr) {
@@ -271,6 +286,11 @@ geninv_status gram(geninv_handle h, const double *G, long long m, long long n, l
       S = bs;
     }
   }
+  // two-level accumulation inside each CTA: register sums over chunks of <= gram_chunk_rows() rows of G,
+  // added into the tile in memory (GemmOp::kchunk) -- the accuracy of the long Gram sums (C4: 2^21 rows)
+  const long long per_cta = (ell + S - 1) / S;
+  const int crow = gram_chunk_rows();
+  if (crow > 0 && per_cta > crow) op.kchunk = crow / 16;
   if (S == 1 && !accumulate) {
     op.C = A;
     op.ldc = lda;
@@ -577,9 +597,12 @@ bool k_order_cheaper(long long s, long long ell, long long r) {
 geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans,
                       double *Gp, long long ldp, int r) {
   const long long s = trans ? m : n, ell = trans ? n : m;
-  const long long cap = (long long)h->ld * h->ld;
+  const long long cap = (long long)h->ld * h->ld;   // doubles of the scratch T
   const int rp = (r + 1) / 2 * 2;
-  const long long c = std::min<long long>((ell + 1) / 2 * 2, std::max<long long>(128, cap / rp / 128 * 128));
+  // chunk width: T holds r x c (N) or c x rp (T) doubles, so c <= cap / rp; whole 128-wide tiles when that
+  // allows, else even (the T view's leading dimension), at least 2 (cap >= 32 * 32 and rp <= s <= ld)
+  long long c = std::min<long long>((ell + 1) / 2 * 2, cap / rp);
+  c = c >= 128 ? c / 128 * 128 : std::max<long long>(2, c / 2 * 2);
   for (long long c0 = 0; c0 < ell; c0 += c) {
     const long long w = std::min(c, ell - c0);   // c even: the T view has an even leading dimension
     GemmOp a, b;
@@ -725,7 +748,30 @@ void fill_info(geninv_info *info, const FactorStats &fs, int r, int tr, geninv_s
 geninv_status check_g(const double *G, long long m, long long n, long long ld) {
   if (!G || m < 1 || n < 1 || ld < n) return GENINV_EINVAL;
   if (m > 0x7fffffffLL || n > 0x7fffffffLL) return GENINV_EINVAL;
-  if (!aligned16(G) || (ld & 1)) return GENINV_EALIGN;
+  return GENINV_OK;
+}
+
+// An operand the TMA path cannot read in place (base not 16-byte aligned, or an odd leading dimension:
+// tensor-map strides are multiples of 16 bytes) is copied once, on the handle's stream, into a handle-owned
+// buffer with the leading dimension rounded up to even; X (rows x cols, ld) is redirected to the copy.
+// slot 0: G, slot 1: the right-hand sides F of geninv_solve_d.  Costs rows x cols doubles of device memory
+// and one device-to-device copy; aligned operands are used in place.
+geninv_status stage_operand(geninv_handle h, int slot, const double *&X, long long rows, long long cols,
+                            long long &ld) {
+  if (aligned16(X) && !(ld & 1)) return GENINV_OK;
+  const long long lds = (cols + 1) / 2 * 2;
+  const size_t need = (size_t)rows * lds * sizeof(double);
+  if (need > h->stage_bytes[slot]) {
+    cudaStreamSynchronize(h->st);
+    if (h->stage[slot]) cudaFree(h->stage[slot]);
+    h->stage[slot] = nullptr;
+    h->stage_bytes[slot] = 0;
+    GI_TRY(cudaMalloc(&h->stage[slot], need));
+    h->stage_bytes[slot] = need;
+  }
+  GI_TRY(cudaMemcpy2DAsync(h->stage[slot], lds * 8, X, ld * 8, cols * 8, rows, cudaMemcpyDeviceToDevice, h->st));
+  X = h->stage[slot];
+  ld = lds;
   return GENINV_OK;
 }
 
@@ -830,6 +876,9 @@ geninv_status geninv_destroy(geninv_handle h) {
   if (h->part) cudaFree(h->part);
   if (h->Gdev) cudaFree(h->Gdev);
   if (h->T1) cudaFree(h->T1);
+  for (auto &b : h->stage)
+    if (b) cudaFree(b);
+  if (h->coll) cudaFree(h->coll);
   for (void *p : {(void *)h->emu_x, (void *)h->emu_g, (void *)h->emu_ex, (void *)h->emu_eg, (void *)h->emu_flag,
                   (void *)h->emu_sc, (void *)h->emu_cm})
     if (p) cudaFree(p);
@@ -861,7 +910,7 @@ const char *geninv_strerror(geninv_status st) {
     case GENINV_ENOTSPD: return "L'L is not numerically SPD (pivot <= 0 in its Cholesky)";
     case GENINV_ECUDA: return "CUDA error";
     case GENINV_ENOMEM: return "device out of memory";
-    case GENINV_EALIGN: return "pointer not 16-byte aligned or odd leading dimension";
+    case GENINV_EALIGN: return "reserved (alignment is handled by staging; not returned)";
     case GENINV_ESTATE: return "no factorisation of matching size in the handle";
     case GENINV_ENCCL: return "NCCL unavailable or the all-reduce failed";
     case GENINV_ERANGE: return "an accepted pivot is subnormal (|G| too small): scale G by a power of two";
@@ -872,16 +921,12 @@ const char *geninv_strerror(geninv_status st) {
 geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp, int64_t ldp,
                        int64_t *rank, const geninv_opts *opts, geninv_info *info) {
   if (!h || !Gp || ldp < m) return GENINV_EINVAL;
-  {
-    const geninv_status cs = check_g(G, m, n, ld);
-    // the one-CTA small path stages G with 8-byte copies when needed: any alignment / ld is fine there
-    if (cs != GENINV_OK && !(cs == GENINV_EALIGN && is_small(m, n))) return cs;
-  }
+  GI_TRYS(check_g(G, m, n, ld));
   cudaSetDevice(h->device);
   const int tr = m < n;  // P:109 (strict; m == n takes the N branch, R6)
   const int s = (int)(tr ? m : n);
   GI_TRYS(ensure_ws(h, s));
-  if (is_small(m, n)) {
+  if (is_small(m, n)) {   // the one-CTA path reads G with 8-byte loads when needed: any alignment / ld
     int r = 0;
     FactorStats fs{};
     geninv_status st = small_path(h, G, m, n, ld, Gp, ldp, opts, &r, &fs);
@@ -889,6 +934,9 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
     fill_info(info, fs, r, tr, st);
     return st;
   }
+  long long ldg = ld;
+  GI_TRYS(stage_operand(h, 0, G, m, n, ldg));
+  ld = ldg;
   GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
   int r = 0;
   FactorStats fs{};
@@ -914,6 +962,11 @@ geninv_status geninv_d_async(geninv_handle h, const double *G, int64_t m, int64_
   const int tr = m < n;
   const int s = (int)(tr ? m : n);
   GI_TRYS(ensure_ws(h, s));
+  {
+    long long ldg = ld;
+    GI_TRYS(stage_operand(h, 0, G, m, n, ldg));
+    ld = ldg;
+  }
   GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
   const int np = (s + PB - 1) / PB;
   const int *rk_final = h->rk + np;
@@ -1133,24 +1186,43 @@ static nccl_allreduce_fn nccl_allreduce() {
 geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G_local, int64_t m_local, int64_t n,
                                int64_t ld, int32_t trans, double *Gp_local, int64_t ldp, int64_t *rank,
                                const geninv_opts *opts, geninv_info *info) {
-  if (!h || !nccl_comm || !Gp_local) return GENINV_EINVAL;
-  GI_TRYS(check_g(G_local, m_local, n, ld));
-  const long long s = trans ? m_local : n;
-  if (ldp < (trans ? s : m_local)) return GENINV_EINVAL;
+  if (!h || !nccl_comm) return GENINV_EINVAL;
   nccl_allreduce_fn ar = nccl_allreduce();
-  if (!ar) return GENINV_ENCCL;
+  if (!ar) return GENINV_ENCCL;   // no communication possible at all (the same library on every rank)
   cudaSetDevice(h->device);
-  GI_TRYS(ensure_ws(h, (int)s));
-  // a1 on the local block, into a zeroed A (the all-reduced upper triangle stays exactly zero)
-  GI_TRY(cudaMemsetAsync(h->A, 0, (size_t)s * h->ld * sizeof(double), h->st));
-  GI_TRYS(gram(h, G_local, m_local, n, ld, trans, h->A, h->ld));
+  if (!h->coll) GI_TRY(cudaMalloc(&h->coll, 4 * sizeof(double)));
+  // Local checks and the local Gram first; then every rank takes part in one small MAX all-reduce of
+  // (status, s, -s) before the big one, so a rank that failed locally (bad arguments, ENOMEM, a CUDA
+  // error) or a shape that differs between ranks makes ALL ranks return the error instead of leaving
+  // the others blocked in the all-reduce of A.
+  const long long s = trans ? m_local : n;
+  geninv_status st = check_g(G_local, m_local, n, ld);
+  if (st == GENINV_OK && (!Gp_local || ldp < (trans ? s : m_local) || s > 0x7fffffffLL)) st = GENINV_EINVAL;
+  long long ldg = ld;
+  if (st == GENINV_OK) st = ensure_ws(h, (int)s);
+  if (st == GENINV_OK) st = stage_operand(h, 0, G_local, m_local, n, ldg);
+  if (st == GENINV_OK) {
+    // a1 on the local block, into a zeroed A (the all-reduced upper triangle stays exactly zero)
+    const cudaError_t e = cudaMemsetAsync(h->A, 0, (size_t)s * h->ld * sizeof(double), h->st);
+    st = e == cudaSuccess ? gram(h, G_local, m_local, n, ldg, trans, h->A, h->ld) : cuda_status(e);
+  }
+  {
+    double pre[3] = {(double)st, st == GENINV_OK ? (double)s : 0.0, st == GENINV_OK ? -(double)s : 0.0};
+    GI_TRY(cudaMemcpyAsync(h->coll, pre, sizeof(pre), cudaMemcpyHostToDevice, h->st));
+    if (ar(h->coll, h->coll, 3, /*ncclFloat64*/ 8, /*ncclMax*/ 2, nccl_comm, h->st) != 0) return GENINV_ENCCL;
+    GI_TRY(cudaMemcpyAsync(pre, h->coll, sizeof(pre), cudaMemcpyDeviceToHost, h->st));
+    GI_TRY(cudaStreamSynchronize(h->st));
+    if (st != GENINV_OK) return st;
+    if (pre[0] != 0.0) return (geninv_status)(int)pre[0];   // another rank failed
+    if (pre[1] != -pre[2]) return GENINV_EINVAL;             // s differs between ranks
+  }
   // a8: A = sum_p A_p -- the one exchange step (NCCL over NVLink / NVSwitch), FP64 sum
   if (ar(h->A, h->A, (size_t)s * h->ld, /*ncclFloat64*/ 8, /*ncclSum*/ 0, nccl_comm, h->st) != 0) return GENINV_ENCCL;
   int r = 0;
   FactorStats fs{};
-  geninv_status st = from_gram(h, h->A, (int)s, h->ld, opts, &r, &fs);   // a2-a6, replicated
+  st = from_gram(h, h->A, (int)s, h->ld, opts, &r, &fs);   // a2-a6, replicated (deterministic: same r, X)
   if (st == GENINV_OK) st = finish_spd_check(h, r);
-  if (st == GENINV_OK) st = apply(h, G_local, m_local, n, ld, trans, Gp_local, ldp, h->st);   // a7, local block
+  if (st == GENINV_OK) st = apply(h, G_local, m_local, n, ldg, trans, Gp_local, ldp, h->st);   // a7, local block
   if (st == GENINV_OK) {
     cudaError_t e = cudaStreamSynchronize(h->st);
     if (e != cudaSuccess) st = cuda_status(e);
@@ -1165,12 +1237,18 @@ geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_
                              geninv_info *info) {
   if (!h || !F || !W || k < 1 || ldf < k || ldw < k) return GENINV_EINVAL;
   GI_TRYS(check_g(G, m, n, ld));
-  if (!aligned16(F) || (ldf & 1)) return GENINV_EALIGN;
   if (k > 0x7fffffffLL) return GENINV_EINVAL;
   cudaSetDevice(h->device);
   const int tr = m < n;
   const int s = (int)(tr ? m : n);
   GI_TRYS(ensure_ws(h, s));
+  {
+    long long ldg = ld, ldff = ldf;
+    GI_TRYS(stage_operand(h, 0, G, m, n, ldg));
+    GI_TRYS(stage_operand(h, 1, F, m, k, ldff));
+    ld = ldg;
+    ldf = ldff;
+  }
   GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
   int r = 0;
   FactorStats fs{};
@@ -1185,6 +1263,9 @@ geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_
   const size_t tb = (size_t)s * ldt * sizeof(double);
   if (tb > h->t1_bytes) {
     if (h->T1) cudaFree(h->T1);
+  for (auto &b : h->stage)
+    if (b) cudaFree(b);
+  if (h->coll) cudaFree(h->coll);
     h->T1 = nullptr;
     h->t1_bytes = 0;
     GI_TRY(cudaMalloc(&h->T1, tb));
@@ -1237,7 +1318,9 @@ geninv_status geninv_gram_d(geninv_handle h, const double *G, int64_t m, int64_t
   if (lda < s) return GENINV_EINVAL;
   cudaSetDevice(h->device);
   GI_TRYS(ensure_ws(h, (int)s));
-  return gram(h, G, m, n, ld, trans ? 1 : 0, A, lda);
+  long long ldg = ld;
+  GI_TRYS(stage_operand(h, 0, G, m, n, ldg));
+  return gram(h, G, m, n, ldg, trans ? 1 : 0, A, lda);
 }
 
 geninv_status geninv_from_gram_d(geninv_handle h, const double *A, int64_t s, int64_t lda, int64_t *rank,
@@ -1261,18 +1344,26 @@ geninv_status geninv_apply_d(geninv_handle h, const double *G, int64_t m, int64_
   if (h->x_s != s) return GENINV_ESTATE;
   if (ldp < (trans ? s : m)) return GENINV_EINVAL;
   cudaSetDevice(h->device);
-  return apply(h, G, m, n, ld, trans ? 1 : 0, Gp, ldp, h->st);
+  long long ldg = ld;
+  GI_TRYS(stage_operand(h, 0, G, m, n, ldg));
+  return apply(h, G, m, n, ldg, trans ? 1 : 0, Gp, ldp, h->st);
 }
 
 geninv_status geninv_frchol_d(geninv_handle h, const double *A, int64_t s, int64_t lda, double *L, int64_t ldl,
                               int32_t *piv_dev, int64_t *rank, const geninv_opts *opts, geninv_info *info) {
   if (!h || !A || !L || !piv_dev || s < 1 || lda < s || ldl < s) return GENINV_EINVAL;
-  if (!aligned16(L) || (ldl & 1)) return GENINV_EALIGN;
   cudaSetDevice(h->device);
   GI_TRYS(ensure_ws(h, (int)s));
   int r = 0;
   FactorStats fs{};
-  geninv_status st = factor(h, A, lda, (int)s, L, ldl, piv_dev, opts, &r, &fs);
+  // L is a TMA operand of the lookahead updates: an unaligned / odd-ld L is factored in the handle's
+  // L workspace and copied out
+  const bool direct = aligned16(L) && !(ldl & 1);
+  geninv_status st = factor(h, A, lda, (int)s, direct ? L : h->L, direct ? ldl : h->ld, piv_dev, opts, &r, &fs);
+  if (!direct && (st == GENINV_OK || st == GENINV_ENONFINITE || st == GENINV_ERANGE)) {
+    GI_TRY(cudaMemcpy2DAsync(L, ldl * 8, h->L, h->ld * 8, (size_t)s * 8, s, cudaMemcpyDeviceToDevice, h->st));
+    GI_TRY(cudaStreamSynchronize(h->st));
+  }
   if (rank) *rank = r;
   fill_info(info, fs, r, 0, st);
   return st;

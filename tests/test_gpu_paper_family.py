@@ -56,5 +56,5 @@ def test_paper_family_batched(H, n):
     for i in range(Gb.shape[0]):
         R = O.geninv(Gb[i].cpu().numpy())
         assert int(rk[i]) == R.rank == 7 * n // 8
-        if R.in_Q():
-            assert C.rel_fro(Gpb[i].cpu().numpy(), R.Gp) <= 1e-9
+        assert R.in_Q()                   # seeds 1..8 are all in Q at n = 32, 64 (tools/screen_q_cpu.py)
+        assert C.rel_fro(Gpb[i].cpu().numpy(), R.Gp) <= 1e-9

@@ -28,17 +28,22 @@ def dev(X):
     return t[:, :n]
 
 
+# seeds: the first seed >= m * 7 + n whose oracle margins are in Q (tools/screen_q_cpu.py)
+SOLVE_SEED = {(300, 130, 70): 2230, (130, 300, 70): 1211, (2050, 530, 400): 14880, (257, 255, 200): 2054,
+              (96, 64, 40): 736, (64, 64, 64): 512}
+
+
 @pytest.mark.parametrize("m,n,r,k", [(300, 130, 70, 1), (130, 300, 70, 7), (2050, 530, 400, 64), (257, 255, 200, 3),
                                      (96, 64, 40, 10), (64, 64, 64, 5)])
 def test_solve_parity(H, m, n, r, k):
-    G = I.low_rank(m * 7 + n, m, n, r).numpy()
+    G = I.low_rank(SOLVE_SEED[(m, n, r)], m, n, r).numpy()
     F = I.dense_normal(m + k, m, k).numpy()
     Wo, ro = O.solve(G, F)
     R = O.geninv(G)
+    assert R.in_Q()
     W, info = H.geninv_solve_d(dev(G), torch.as_tensor(F).cuda())
-    assert info.rank == ro
-    if R.in_Q():
-        assert C.rel_fro(W.cpu().numpy(), Wo) <= 1e-9
+    assert info.rank == ro == r
+    assert C.rel_fro(W.cpu().numpy(), Wo) <= 1e-9
 
 
 def test_solve_tall_split_k(H):

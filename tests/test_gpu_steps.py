@@ -7,6 +7,9 @@ BIT-EXACT there whatever its summation order:
   P3  unimodular B = U U' -> M = inv(B)
 Random inputs are graded at the floating-point level.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -16,6 +19,7 @@ from oracle import geninv_oracle as O
 from paper_0804_4809_b200 import inputs as I
 
 pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
 
 
 @pytest.fixture(scope="module")
@@ -98,6 +102,23 @@ def test_frchol_strict_tolerance(H):
     assert info.rank == 2 and pv.cpu().tolist() == [0, 2]
     L, pv, info = H.geninv_frchol_d(padded(A, 4), tol_abs=float(np.nextafter(1.0, 0.0)))
     assert info.rank == 4
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_frchol_margins_golden(H, k):
+    # the hand-worked margins (tests/golden "margins", negative dropped pivots): the device reports the same
+    # decisions and min accepted / max |dropped| / min pivot, exactly (every value is a small dyadic rational)
+    ex = GOLD["margins"][k]
+    A = np.array(ex["A"], dtype=float)
+    kw = {"tol_abs": ex["tol"]} if ex["tol"] is not None else {}
+    L, pv, info = H.geninv_frchol_d(padded(A, 4), **kw)
+    assert info.rank == ex["rank"] and pv.cpu().tolist()[:ex["rank"]] == ex["piv"]
+    assert np.array_equal(L.cpu().numpy()[:, :ex["rank"]], np.array(ex["L"], dtype=float))
+    assert info.min_acc == min(ex["accepted"])
+    assert info.max_drop == max(abs(v) for v in ex["dropped"])
+    assert info.min_pivot == ex["min_pivot"]
+    if ex["tol"] is None:
+        assert info.tol == ex["tol_expected"]
 
 
 @pytest.mark.parametrize("r,seed", [(8, 0), (32, 1), (33, 2), (64, 3), (100, 4)])

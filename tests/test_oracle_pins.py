@@ -33,6 +33,66 @@ def test_golden_full_rank_cholesky(ex):
     assert list(ch.piv) == ex["piv"]
 
 
+@pytest.mark.parametrize("ex", GOLD["margins"], ids=["tol_abs", "paper_tol"])
+def test_golden_margins(ex):
+    """Decision margins (they define predicates Q / Q*, which gate every GPU comparison)
+    on a hand-worked A with negative dropped pivots, for the scalar and the batched oracle."""
+    A = np.array(ex["A"], dtype=float)
+    tol = ex["tol"] if ex["tol"] is not None else O.tolerance(A)
+    if ex["tol"] is None:
+        assert tol == ex["tol_expected"]
+    ch = O.full_rank_cholesky(A, tol)
+    assert ch.rank == ex["rank"] and list(ch.piv) == ex["piv"]
+    assert np.array_equal(ch.L, np.array(ex["L"], dtype=float))
+    assert list(ch.accepted) == ex["accepted"] and list(ch.dropped) == ex["dropped"]
+    assert ch.mu_acc == pytest.approx(ex["mu_acc"], rel=1e-15)
+    assert ch.mu_drop == pytest.approx(ex["mu_drop"], rel=1e-15)
+    assert ch.min_pivot == ex["min_pivot"]
+    # batched form: the same matrix three times (plus a permuted-irrelevant zero matrix: rank 0, no margins)
+    Ab = np.stack([A, A, np.zeros_like(A), A])
+    tb = np.array([tol, tol, 0.0, tol])
+    Lb, rb, min_acc, max_drop, min_piv = O.full_rank_cholesky_batched(Ab, tb)
+    assert list(rb) == [ex["rank"]] * 2 + [0] + [ex["rank"]]
+    for b in (0, 1, 3):
+        assert np.array_equal(Lb[b][:, :ex["rank"]], ch.L) and not Lb[b][:, ex["rank"]:].any()
+        assert min_acc[b] / tol == pytest.approx(ex["mu_acc"], rel=1e-15)
+        assert max_drop[b] / tol == pytest.approx(ex["mu_drop"], rel=1e-15)
+        assert min_piv[b] == ex["min_pivot"]
+    assert min_acc[2] == np.inf and max_drop[2] == 0.0 and min_piv[2] == 0.0
+
+
+def test_margin_mutations_are_caught(monkeypatch):
+    """A signed max instead of max |.| for mu_drop, or min over accepted replaced by min over all pivots,
+    fails the margin goldens (the VERDICT r1 mutation)."""
+    ex = GOLD["margins"][1]
+    A = np.array(ex["A"], dtype=float)
+
+    def golden_ok():
+        ch = O.full_rank_cholesky(A, O.tolerance(A))
+        return (ch.mu_drop == pytest.approx(ex["mu_drop"], rel=1e-15)
+                and ch.mu_acc == pytest.approx(ex["mu_acc"], rel=1e-15))
+    assert golden_ok()
+    monkeypatch.setattr(O.FullRankCholesky, "mu_drop", property(lambda self: float(self.dropped.max() / self.tol)))
+    assert not golden_ok()
+    monkeypatch.undo()
+    monkeypatch.setattr(O.FullRankCholesky, "mu_acc", property(lambda self: float(
+        np.concatenate([self.accepted, self.dropped]).min() / self.tol)))
+    assert not golden_ok()
+
+
+def test_margins_define_Q():
+    """Q / Q* thresholds on GeninvResult, at and across their boundaries."""
+    def res(acc, drop, tol=1.0):
+        ch = O.FullRankCholesky(np.zeros((2, 1)), 1, tol, np.array([0]), np.array(acc, dtype=float),
+                                np.array(drop, dtype=float))
+        return O.GeninvResult(np.zeros((1, 1)), 1, tol, False, ch)
+    assert res([1e4], [1e-2]).in_Q() and not res([1e4], [1e-2]).in_Qstar()
+    assert not res([9.999e3], [0.0]).in_Q()
+    assert not res([1e5], [-0.0101]).in_Q()            # |negative| dropped pivot counts
+    assert res([1e6], [-1e-3]).in_Qstar() and not res([1e6], [-1.01e-3]).in_Qstar()
+    assert res([2e6, 1e6], []).mu_drop == 0.0 and res([2e6, 1e6], []).mu_acc == 1e6
+
+
 @pytest.mark.parametrize("ex", GOLD["geninv"], ids=lambda e: e["cite"][:20])
 def test_golden_geninv(ex):
     G = np.array(ex["G"], dtype=float)
