@@ -222,6 +222,14 @@ int upd_tile_bm() {
 
 cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
   if (op.M <= 0 || op.N <= 0) return cudaSuccess;
+  static const bool dbg = getenv("GENINV_DEBUG_GEMM") != nullptr;   // diagnostics: one line per launch
+  if (dbg)
+    fprintf(stderr,
+            "gemm M=%d N=%d K=%d A=%p ld=%lld %lldx%lld %s mn0=%d k0=%d | B=%p ld=%lld %lldx%lld %s mn0=%d k0=%d | "
+            "C=%p ldc=%lld splits=%d lower=%d kchunk=%d\n",
+            op.M, op.N, op.K, (const void *)op.A.ptr, op.A.ld, op.A.rows, op.A.cols, op.a_kmajor ? "K" : "MN", op.a_mn0,
+            op.a_k0, (const void *)op.B.ptr, op.B.ld, op.B.rows, op.B.cols, op.b_kmajor ? "K" : "MN", op.b_mn0, op.b_k0,
+            (void *)op.C, op.ldc, op.splits, (int)op.lower, op.kchunk);
   if (op.lower && op.M != op.N) return cudaErrorInvalidValue;
   GemmArgs a;
   memset(&a, 0, sizeof(a));

@@ -90,6 +90,19 @@ geninv_status cuda_status(cudaError_t e) {
     }                                                                            \
   } while (0)
 
+// GENINV_DEBUG_SYNC: synchronise the device after a step and report the first failing one (diagnostics)
+bool debug_sync_on() {
+  static const bool on = getenv("GENINV_DEBUG_SYNC") != nullptr;
+  return on;
+}
+#define GI_DBG_SYNC(tag)                                                                        \
+  do {                                                                                          \
+    if (debug_sync_on()) {                                                                      \
+      cudaError_t _e = cudaDeviceSynchronize();                                                 \
+      fprintf(stderr, "[geninv] sync after %s: %s\n", tag, cudaGetErrorString(_e));            \
+    }                                                                                           \
+  } while (0)
+
 #define GI_TRYS(expr)                                 \
   do {                                                \
     geninv_status _s = (expr);                        \
@@ -329,8 +342,13 @@ geninv_status gemm_splitk(geninv_handle h, GemmOp op) {
   op.ldc = op.N;
   op.splits = S;
   op.split_stride = pstride;
+  if (debug_sync_on())
+    fprintf(stderr, "[geninv] gemm_splitk: part %p (%zu B) S %d pstride %lld -> C %p ldc %lld\n", (void *)h->part,
+            h->part_bytes, S, pstride, (void *)C, ldc);
   GI_TRY(gemm(op, h->st));
+  GI_DBG_SYNC("gemm_splitk: gemm");
   GI_TRY(splitk_reduce(h->part, pstride, S, op.N, C, ldc, nullptr, 0, 1.0, op.M, op.N, false, h->st));
+  GI_DBG_SYNC("gemm_splitk: reduce");
   h->launches += 2;
   return GENINV_OK;
 }
@@ -1249,10 +1267,13 @@ geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_
     ld = ldg;
     ldf = ldff;
   }
+  GI_DBG_SYNC("solve: staging");
   GI_TRYS(gram(h, G, m, n, ld, tr, h->A, h->ld));
+  GI_DBG_SYNC("solve: gram");
   int r = 0;
   FactorStats fs{};
   geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs);
+  GI_DBG_SYNC("solve: from_gram");
   if (st == GENINV_OK) st = finish_spd_check(h, r);
   if (st != GENINV_OK) {
     if (rank) *rank = r;
@@ -1263,9 +1284,6 @@ geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_
   const size_t tb = (size_t)s * ldt * sizeof(double);
   if (tb > h->t1_bytes) {
     if (h->T1) cudaFree(h->T1);
-  for (auto &b : h->stage)
-    if (b) cudaFree(b);
-  if (h->coll) cudaFree(h->coll);
     h->T1 = nullptr;
     h->t1_bytes = 0;
     GI_TRY(cudaMalloc(&h->T1, tb));
@@ -1301,7 +1319,9 @@ geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_
     b.M = (int)n; b.N = (int)k; b.K = s;
     b.C = W; b.ldc = ldw;
   }
+  GI_DBG_SYNC("solve: T1");
   GI_TRYS(gemm_splitk(h, a));
+  GI_DBG_SYNC("solve: first product");
   GI_TRYS(gemm_splitk(h, b));
   cudaError_t e = cudaStreamSynchronize(h->st);
   if (e != cudaSuccess) st = cuda_status(e);
