@@ -444,3 +444,34 @@ def _frc_variant(A, tol, sign=-1, geq=False, scale=True):
         else:
             drop.append(c[0])
     return O.FullRankCholesky(L[:, :r].copy(), r, tol, np.array(piv, dtype=np.int64), np.array(acc), np.array(drop))
+
+
+# ------------------------------------------- oracle/extended.py (the spread reference, reading R23)
+def test_extended_integer_exact_and_branches():
+    from oracle import extended as E
+    Lt, piv = integer_ltrue(30, 12, 3)
+    G = np.vstack([Lt.T, np.zeros((5, 30))])          # G'G = Lt Lt' exactly; 17 x 30: transpose branch
+    Gt = np.ascontiguousarray(G.T)                    # 30 x 17: N branch, Gram = G G' of the above
+    for ge, ce in ((True, True), (True, False), (False, True)):
+        Y, r, tol = E.geninv_ext(Gt, ge, ce)
+        R = O.geninv(Gt)
+        assert r == R.rank == 12 and tol == R.tol
+        assert C.rel_fro(Y, R.Gp) <= 1e-12
+        Yt, rt, _ = E.geninv_ext(G, ge, ce)
+        assert rt == 12 and C.rel_fro(Yt, O.geninv(G).Gp) <= 1e-12
+
+
+def test_extended_matches_oracle_well_conditioned_and_beats_it_ill_conditioned():
+    from oracle import extended as E
+    G = I.dense_normal(5, 120, 40).numpy()               # cond ~ 3: both evaluations agree to rounding
+    assert C.rel_fro(E.geninv_ext(G)[0], O.geninv(G).Gp) <= 1e-13
+    # ill-conditioned accepted columns (C5 shape): the extended Gram + Cholesky is at least as close to the
+    # SVD pseudoinverse as the FP64 oracle on average over a few matrices
+    Gb = I.make_batch(I.CONFIGS["C5"], 3, 0, 24).numpy()
+    e_fp64, e_ext = [], []
+    for G in Gb:
+        R = O.geninv(G)
+        P = np.linalg.pinv(G, rcond=1e-10)
+        e_fp64.append(C.rel_fro(R.Gp, P))
+        e_ext.append(C.rel_fro(E.geninv_ext(G)[0], P))
+    assert np.median(e_ext) <= np.median(e_fp64) * 1.5
