@@ -173,6 +173,11 @@ def dist_setup(n_gpus: int):
             raise SystemExit(f"--gpus {n_gpus} needs torchrun --nproc-per-node {n_gpus}")
     if world > 1:
         import torch.distributed as dist
+        # the one exchange (the all-reduce of A) pinned to one algorithm / protocol: its summation order is
+        # then fixed run to run as well as identical on every rank (the replicated factorisation needs
+        # bit-identical A); at ~0.1-0.3 ms against seconds of DMMA work the choice costs nothing
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
@@ -254,6 +259,61 @@ def run_oracle_once(G):
     return fl, dt
 
 
+def host_record():
+    """The box's host CPU and the oracle's thread settings."""
+    rec = {"cpu_model": None, "sockets": None, "cores_per_socket": None, "threads_per_core": None,
+           "logical_cpus_usable": cpu_cores(), "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+           "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            v = v.strip()
+            if k == "Model name":
+                rec["cpu_model"] = v
+            elif k == "Socket(s)":
+                rec["sockets"] = int(v)
+            elif k == "Core(s) per socket":
+                rec["cores_per_socket"] = int(v)
+            elif k == "Thread(s) per core":
+                rec["threads_per_core"] = int(v)
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        rec["blas"] = [{"api": d.get("internal_api"), "threads": d.get("num_threads")} for d in threadpool_info()
+                       if d.get("user_api") == "blas"]
+    except Exception:
+        rec["blas"] = None
+    return rec
+
+
+def oracle_extra_times(dev):
+    """1-thread oracle times for C1 and a 1024-matrix C5 slice, and the all-thread oracle on the FULL C3
+    (SURVEY §8(d5)); inputs from the same generator (C3 formed on the device, as the bench's input)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import geninv_oracle as O
+    out = {}
+    G1 = I.make_single(I.CONFIGS["C1"], seed_of(I.CONFIGS["C1"])).numpy()
+    G5 = I.make_batch(I.CONFIGS["C5"], seed_of(I.CONFIGS["C5"]), 0, 1024).numpy()
+    with threadpool_limits(limits=1):
+        O.geninv(G1)
+        t0 = time.perf_counter()
+        for _ in range(20):
+            O.geninv(G1)
+        out["C1_1thread_ms"] = (time.perf_counter() - t0) / 20 * 1e3
+        t0 = time.perf_counter()
+        O.geninv_batched(G5)
+        out["C5_1024_matrices_1thread_s"] = time.perf_counter() - t0
+    c3 = I.CONFIGS["C3"]
+    G3 = I.make_single(c3, seed_of(c3), device=dev).cpu().numpy()
+    t0 = time.perf_counter()
+    O.geninv(G3)
+    out["C3_full_all_threads_s"] = time.perf_counter() - t0
+    return out
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -280,7 +340,8 @@ def reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt_tot / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "sample": sample},
-            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle", "sample": sample,
+                             "host": host_record()},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -303,7 +364,7 @@ def main():
         return reference_arm(args)
 
     from paper_0804_4809_b200.binding import Handle
-    from paper_0804_4809_b200.sharded import CudaBackend, row_range
+    from paper_0804_4809_b200.sharded import row_range
 
     world, rank, local = dist_setup(args.gpus)
     cfg, c3t, desc = workload(args.workload)
@@ -337,56 +398,33 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-    ev_out = []
-    ev_phase = []
+    trans = 1 if colshard else tr
+    comm = None
+    if world > 1:
+        t_ = torch.ones(1, device=dev)
+        dist.all_reduce(t_)                          # creates the NCCL communicator
+        comm = dist.distributed_c10d._get_default_group()._get_backend(dev)._comm_ptr()
 
-    def ev():
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(stream)
-        return e
-
-    be = CudaBackend(h, trans=1 if colshard else 0)
-    # the whole call geninv_d (the user's API) for the single-GPU configs; C4 / C3T keep the split form
-    # so the phases (Gram + all-reduce, factorisation, output) are timed separately at every N
-    whole = bool(world == 1 and cfg.name in ("C1", "C2", "C3"))
-
-    def step(record=False):
-        # the sharded step of paper_0804_4809_b200/sharded.py, with events between its stages
-        if record:
-            p0 = ev()
-        if whole:
-            info = None
+    # The timed step is the product entry point a user calls: geninv_d (N = 1) or geninv_sharded_d
+    # (N > 1: local Gram, ncclAllReduce of A inside the library, replicated factorisation, local block of
+    # G+).  The phases and the a7 launch (the roofline kernel) are timed in separate untimed passes below.
+    def step():
+        if world > 1:
+            _, info = h.geninv_sharded_d(comm, G, 1 if colshard else 0, Gp)
         else:
-            be.gram(G, A)                            # a1 on the local rows
-            be.all_reduce(A)                         # a8: A = sum_p G_p'G_p (NCCL over NVLink; no-op at N = 1)
-            p1 = ev() if record else None
-            info = be.from_gram(A)                   # a2-a6, replicated
-        if whole:                                    # T branch (single GPU): whole call
             _, info = h.geninv_d(G, Gp)
-            return info
-        if record:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        be.apply(G, Gp)                              # a7: local column (C3: row) block of G+
-        if record:
-            e1.record(stream)
-            ev_out.append((e0, e1))
-            ev_phase.append((p0, p1, e0, e1))
         return info
 
     info = step()
     torch.cuda.synchronize()
-    # piv for the flop model (untimed): the full-rank Cholesky of the same A
-    if not whole:
-        _, piv, _ = h.geninv_frchol_d(A)
-        piv = piv.cpu().numpy()
-    else:
-        Aw = torch.zeros(s, s, dtype=torch.float64, device=dev)
-        h.geninv_gram_d(G, tr, Aw)
-        _, piv, _ = h.geninv_frchol_d(Aw)
-        piv = piv.cpu().numpy()
-        del Aw
+    # piv for the flop model (untimed): the full-rank Cholesky of the (all-reduced) Gram
+    Aw = torch.zeros(s, s, dtype=torch.float64, device=dev)
+    h.geninv_gram_d(G, trans, Aw)
+    if world > 1:
+        dist.all_reduce(Aw)
+    _, piv, _ = h.geninv_frchol_d(Aw)
+    piv = piv.cpu().numpy()
+    del Aw
     F = f_alg(s, ell, piv)
     for _ in range(max(0, args.warmup - 1)):
         step()
@@ -406,15 +444,15 @@ def main():
                 fbuf.fill_(1.0)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                info = step(record=True)
+                info = step()
                 b.record(stream)
                 step_ev.append((a, b))
             else:
-                info = step(record=True)
+                info = step()
         t1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
-    launches = (h.launch_count - l0) * world + (args.steps * world if world > 1 else 0)  # + NCCL all-reduce
+    launches = (h.launch_count - l0) * world + (2 * args.steps * world if world > 1 else 0)  # + 2 NCCL all-reduces
     if flush:
         ms = float(sum(a.elapsed_time(b) for a, b in step_ev)) / args.steps
     else:
@@ -422,42 +460,62 @@ def main():
     ms = allmax(ms, world)
     value = F["total"] / (ms * 1e-3) / 1e9
     peak, peak_src = fp64_peak()
-    # dominant kernel: a7 output product, one launch per step per rank.  Whole-call configs (the a7
-    # launch is inside geninv_d) time the same launch through geninv_apply_d right after the timed
-    # region: K launches on the same X and G, each between CUDA events on the launching stream
-    roof_note = "a7 launches of the timed steps (CUDA events around each on the launching stream)"
-    if whole:
-        Gp_ap = torch.empty(n, m, dtype=torch.float64, device=dev)
-        try:
-            for _ in range(args.steps):
-                if flush:
-                    fbuf.fill_(1.0)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                h.geninv_apply_d(G, tr, Gp_ap)
-                e1.record(stream)
-                ev_out.append((e0, e1))
-            torch.cuda.synchronize()
-            roof_note = ("geninv_apply_d (the same a7 launch geninv_d makes, on the X the timed calls left) x "
-                         "steps after the timed region, CUDA events around each")
-        except Exception as exc:   # the one-CTA small path (C1) keeps no X: its kernel is the batched one
-            ev_out.clear()
-            roof_note = f"not separable: {str(exc)[:120]}"
-        del Gp_ap
+    # cross-rank check of the replicated factorisation: every rank's (r, hash of X's bits) must agree
+    replicated = None
+    if world > 1:
+        from paper_0804_4809_b200.sharded import check_replicated, replicated_digest
+        if info.order == 0:
+            replicated = bool(check_replicated(replicated_digest(h.geninv_copy_x(), info.rank)))
+            if not replicated:
+                raise SystemExit("replicated factorisation differs between ranks (r or X bits)")
+    # dominant kernel: the a7 output product.  geninv_d / geninv_sharded_d launch it inside the call, so the
+    # same launch is timed through geninv_apply_d right after the timed region: `steps` launches on the X the
+    # timed calls left, each between CUDA events on the launching stream (the L2 flushed before each when the
+    # inputs fit in it)
+    roof_note = ("geninv_apply_d (the a7 launch geninv_d / geninv_sharded_d make, on the X the timed calls "
+                 "left) x steps after the timed region, CUDA events around each on the launching stream")
+    ev_out = []
+    try:
+        for _ in range(args.steps):
+            if flush:
+                fbuf.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            h.geninv_apply_d(G, trans, Gp)
+            e1.record(stream)
+            ev_out.append((e0, e1))
+        torch.cuda.synchronize()
+    except Exception as exc:   # the one-CTA small path (C1) and the low-rank K order keep no X
+        ev_out.clear()
+        roof_note = f"not separable: {str(exc)[:120]}"
     if ev_out:
         out_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_out]))
         out_ms = allmax(out_ms, world)
-        out_flops_launch = 2.0 * s * s * (rows if not whole else ell)
-        if info is not None and getattr(info, "order", 0) == 1:   # low-rank K order: K (K'G'), 4 r s ell
-            out_flops_launch = 4.0 * info.rank * s * (rows if not whole else ell)
+        out_flops_launch = 2.0 * s * s * (ell if (tr and not colshard) else rows)   # this rank's long-side lines
         achieved = out_flops_launch / (out_ms * 1e-3) / 1e12
     else:
         out_ms, achieved, out_flops_launch = None, None, None
+    # phases (one untimed pass of the split form, CUDA events between the stages; N > 1: torch's all-reduce)
     phases = None
-    if ev_phase:
-        ph = np.array([[a.elapsed_time(b), b.elapsed_time(c), c.elapsed_time(d)] for a, b, c, d in ev_phase])
-        phases = dict(zip(["gram_allreduce_ms", "factor_inverse_x_ms", "output_ms"], ph.mean(axis=0).round(3).tolist()))
+    try:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        A.zero_()
+        torch.cuda.synchronize()
+        evs[0].record(stream)
+        h.geninv_gram_d(G, trans, A)
+        if world > 1:
+            dist.all_reduce(A)
+        evs[1].record(stream)
+        h.geninv_from_gram_d(A)
+        evs[2].record(stream)
+        h.geninv_apply_d(G, trans, Gp)
+        evs[3].record(stream)
+        torch.cuda.synchronize()
+        phases = dict(zip(["gram_allreduce_ms", "factor_inverse_x_ms", "output_ms"],
+                          [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(3)]))
+    except Exception as exc:
+        phases = {"not separable": str(exc)[:120]}
     traffic = None
     try:
         tr_d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -480,7 +538,7 @@ def main():
     del G, Gp
     torch.cuda.empty_cache()
     if Gh is not None:
-        e2e = e2e_run(args, Gh, gp_shape, int(colshard), world, local, F, h)
+        e2e = e2e_run(args, Gh, gp_shape, int(colshard), world, local, F, h, comm)
         del Gh
 
     cpu = None
@@ -489,7 +547,12 @@ def main():
         fl, dt = run_oracle_once(Gs)                      # warm (BLAS threads, page-in)
         fl, dt = run_oracle_once(Gs)
         cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": sample + f"; oracle = numpy/OpenBLAS geninv of PAPER.md P:105-140, {dt:.2f} s"}
+               "sample": sample + f"; oracle = numpy/OpenBLAS geninv of PAPER.md P:105-140, {dt:.2f} s",
+               "host": host_record()}
+        try:
+            cpu["extra_times"] = oracle_extra_times(dev)
+        except Exception as exc:
+            cpu["extra_times"] = {"skipped": str(exc)[:160]}
 
     if rank == 0:
         i8_peak, i8_src = int8_peak(ms > 1000.0)
@@ -518,6 +581,7 @@ def main():
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": launches,
+            "replicated_check": replicated,
             "roofline": ({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                           "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                           "kernel": "dgemm_tc<128,128,64,32,6,K-major,K-major> (a7 G+ = X G')",
@@ -539,7 +603,7 @@ def main():
     return 0
 
 
-def e2e_run(args, Gh, gp_shape, trans, world, local, F, h):
+def e2e_run(args, Gh, gp_shape, trans, world, local, F, h, comm=None):
     """Same metric through the C ABI with HOST buffers (pinned): the H2D copy of this rank's G and the
     D2H copy of its block of G+ are inside the timed region, every step."""
     dev = torch.device("cuda", local)
@@ -552,16 +616,10 @@ def e2e_run(args, Gh, gp_shape, trans, world, local, F, h):
         import torch.distributed as dist
         Gd = torch.empty(Gh.shape, dtype=torch.float64, device=dev)
         Gpd = torch.empty(gp_shape, dtype=torch.float64, device=dev)
-        s = Gh.shape[0] if trans else Gh.shape[1]
-        A = torch.zeros(s, s, dtype=torch.float64, device=dev)
 
         def step():
             Gd.copy_(Gh, non_blocking=True)
-            A.zero_()
-            h.geninv_gram_d(Gd, trans, A)
-            dist.all_reduce(A)
-            h.geninv_from_gram_d(A)
-            h.geninv_apply_d(Gd, trans, Gpd)
+            h.geninv_sharded_d(comm, Gd, trans, Gpd)
             Gph.copy_(Gpd, non_blocking=True)
             torch.cuda.synchronize()
     else:
@@ -582,7 +640,7 @@ def e2e_run(args, Gh, gp_shape, trans, world, local, F, h):
     return {"value": F["total"] / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms,
             "h2d_bytes_per_step": nbytes_in, "d2h_bytes_per_step": nbytes_out,
             "api": "geninv_host_d (pinned host G and G+)" if world == 1 else
-            "pinned H2D + geninv_gram_d / all_reduce / geninv_from_gram_d / geninv_apply_d + D2H"}
+            "pinned H2D of the local rows + geninv_sharded_d + D2H of the local block of G+"}
 
 
 def bench_batched(args, cfg, desc, world, rank):
@@ -659,7 +717,8 @@ def bench_batched(args, cfg, desc, world, rank):
         fl, dt = run_oracle_once(Gs)
         fl, dt = run_oracle_once(Gs)
         cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": sample + f"; oracle = numpy batched geninv (P:105-140 per matrix), {dt:.2f} s"}
+               "sample": sample + f"; oracle = numpy batched geninv (P:105-140 per matrix), {dt:.2f} s",
+               "host": host_record()}
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <vector>
@@ -72,6 +73,15 @@ struct geninv_handle_s {
 };
 
 namespace {
+
+// NVTX range per step (SURVEY §5 tracing): visible in nsys / ncu --nvtx timelines; a no-op (one call into the
+// NVTX stub) when no tool is attached.
+struct Range {
+  explicit Range(const char *name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range &) = delete;
+  Range &operator=(const Range &) = delete;
+};
 
 geninv_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return GENINV_OK;
@@ -261,6 +271,7 @@ int gram_chunk_rows() {
 // a1: A (s x s, lower) = G'G (trans == 0) or GG' (trans == 1).
 geninv_status gram(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *A,
                    long long lda, const double *accumulate = nullptr) {
+  Range rg("geninv a1 gram");
   const long long s = trans ? m : n, ell = trans ? n : m;
   // emulated Gram: only where its 128 x 256 lower tiles fill the machine (s >= 3072: >= 170 tiles);
   // an accumulating call could not fall back after a range flag
@@ -411,6 +422,7 @@ long long dbits(double x) {
 
 geninv_status factor(geninv_handle h, const double *A, long long lda, int s, double *L, long long ldl, int *piv,
                      const geninv_opts *opts, int *rank_out, FactorStats *hst) {
+  Range rg("geninv a2-a3 tolerance + full-rank Cholesky");
   const long long key[10] = {(long long)(uintptr_t)A, lda, s, (long long)(uintptr_t)L, ldl, (long long)(uintptr_t)piv,
                              dbits(tol_rel_of(opts)), dbits(tol_abs_of(opts)), h->ld, 1};
   GI_TRYS(run_graph(h, h->g_factor, key, [&](cudaStream_t st) -> geninv_status {
@@ -614,6 +626,7 @@ bool k_order_cheaper(long long s, long long ell, long long r) {
 //   N: T (r x c) = K' G[j0:j0+c]',  G+[:, j0:j0+c] = K T;   T: T (c x r) = G[:, i0:i0+c]' K,  G+[i0:i0+c, :] = T K'
 geninv_status apply_k(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans,
                       double *Gp, long long ldp, int r) {
+  Range rg("geninv a7 output (K order)");
   const long long s = trans ? m : n, ell = trans ? n : m;
   const long long cap = (long long)h->ld * h->ld;   // doubles of the scratch T
   const int rp = (r + 1) / 2 * 2;
@@ -720,6 +733,7 @@ geninv_status apply_emulated(geninv_handle h, const double *G, long long m, long
 
 geninv_status apply(geninv_handle h, const double *G, long long m, long long n, long long ld, int trans, double *Gp,
                     long long ldp, cudaStream_t st) {
+  Range rg("geninv a7 output");
   const long long s = trans ? m : n;
   if (emulation_on(h) && s <= 16384) {
     const geninv_status es = apply_emulated(h, G, m, n, ld, trans, Gp, ldp, st);
@@ -805,6 +819,7 @@ geninv_status from_gram(geninv_handle h, const double *A, int s, long long lda, 
   if (k_order) *k_order = ko;
   // a4-a6 (L'L, the SPD inverse's panel chain, TRTRI, the products) as one CUDA graph per (s, r)
   GI_TRYS(prepare_chain(h, s, r, !ko));
+  Range rg("geninv a4-a6 L'L, inverse, K, X");
   const long long key[10] = {s, r, ko ? 0 : 1, h->ld, (long long)(uintptr_t)h->L, 2, (long long)(uintptr_t)h->part,
                              0, 0, 0};
   GI_TRYS(run_graph(h, h->g_build, key, [&](cudaStream_t st) -> geninv_status {
@@ -938,6 +953,7 @@ const char *geninv_strerror(geninv_status st) {
 
 geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp, int64_t ldp,
                        int64_t *rank, const geninv_opts *opts, geninv_info *info) {
+  Range rg_call("geninv_d");
   if (!h || !Gp || ldp < m) return GENINV_EINVAL;
   GI_TRYS(check_g(G, m, n, ld));
   cudaSetDevice(h->device);
@@ -974,6 +990,7 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
 
 geninv_status geninv_d_async(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, double *Gp,
                              int64_t ldp, int64_t *rank_dev, const geninv_opts *opts) {
+  Range rg_call("geninv_d_async");
   if (!h || !Gp || !rank_dev || ldp < m) return GENINV_EINVAL;
   GI_TRYS(check_g(G, m, n, ld));
   cudaSetDevice(h->device);
@@ -1021,6 +1038,7 @@ geninv_status geninv_d_async(geninv_handle h, const double *G, int64_t m, int64_
 
 geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, int64_t n, int64_t ld, double *Gp_host,
                             int64_t ldp, int64_t *rank, const geninv_opts *opts, geninv_info *info) {
+  Range rg_call("geninv_host_d");
   if (!h || !G_host || !Gp_host || m < 1 || n < 1 || ld < n || ldp < m) return GENINV_EINVAL;
   cudaSetDevice(h->device);
   const int tr = m < n;
@@ -1178,6 +1196,7 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
 geninv_status geninv_batched_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, int64_t strideG,
                                int64_t batch, double *Gp, int64_t ldp, int64_t strideGp, int32_t *rank_dev,
                                const geninv_opts *opts) {
+  Range rg_call("geninv_batched_d");
   if (!h || batch < 0 || m < 1 || n < 1 || ld < n || ldp < m) return GENINV_EINVAL;
   if (batch == 0) return GENINV_OK;
   if (!G || !Gp || !rank_dev) return GENINV_EINVAL;
@@ -1204,6 +1223,7 @@ static nccl_allreduce_fn nccl_allreduce() {
 geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G_local, int64_t m_local, int64_t n,
                                int64_t ld, int32_t trans, double *Gp_local, int64_t ldp, int64_t *rank,
                                const geninv_opts *opts, geninv_info *info) {
+  Range rg_call("geninv_sharded_d");
   if (!h || !nccl_comm) return GENINV_EINVAL;
   nccl_allreduce_fn ar = nccl_allreduce();
   if (!ar) return GENINV_ENCCL;   // no communication possible at all (the same library on every rank)
@@ -1235,7 +1255,10 @@ geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G
     if (pre[1] != -pre[2]) return GENINV_EINVAL;             // s differs between ranks
   }
   // a8: A = sum_p A_p -- the one exchange step (NCCL over NVLink / NVSwitch), FP64 sum
-  if (ar(h->A, h->A, (size_t)s * h->ld, /*ncclFloat64*/ 8, /*ncclSum*/ 0, nccl_comm, h->st) != 0) return GENINV_ENCCL;
+  {
+    Range rg("geninv a8 all-reduce of A");
+    if (ar(h->A, h->A, (size_t)s * h->ld, /*ncclFloat64*/ 8, /*ncclSum*/ 0, nccl_comm, h->st) != 0) return GENINV_ENCCL;
+  }
   int r = 0;
   FactorStats fs{};
   st = from_gram(h, h->A, (int)s, h->ld, opts, &r, &fs);   // a2-a6, replicated (deterministic: same r, X)
@@ -1253,6 +1276,7 @@ geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G
 geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_t n, int64_t ld, const double *F,
                              int64_t k, int64_t ldf, double *W, int64_t ldw, int64_t *rank, const geninv_opts *opts,
                              geninv_info *info) {
+  Range rg_call("geninv_solve_d");
   if (!h || !F || !W || k < 1 || ldf < k || ldw < k) return GENINV_EINVAL;
   GI_TRYS(check_g(G, m, n, ld));
   if (k > 0x7fffffffLL) return GENINV_EINVAL;

@@ -45,6 +45,49 @@ def sharded_geninv(backend, G_local, A, Gp_local) -> ShardResult:
     return ShardResult(backend.rank_of(info), info, Gp_local)
 
 
+def batch_range(batch: int, world: int, rank: int):
+    """C5 (independent matrices): rank p owns matrices [b0, b1) -- no exchange at all."""
+    return row_range(batch, world, rank)
+
+
+_PHI = -7046029254386353131        # 0x9E3779B97F4A7C15 as int64
+_M1 = -4658895280553007687         # 0xBF58476D1CE4E5B9
+_M2 = -7723592293110705685         # 0x94D049BB133111EB
+
+
+def _srl(z, k):
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def replicated_digest(X, r: int):
+    """(r, 64-bit hash of X's bits) as 4 exactly representable float64 values (r, then 3 x 22-bit pieces).
+    The hash mixes every element with its position (splitmix64 finaliser), so any differing bit of the
+    replicated X = L M M L' changes it.  Works on CPU and CUDA tensors."""
+    import torch
+    b = X.contiguous().view(-1).view(torch.int64)
+    z = b + (torch.arange(1, b.numel() + 1, dtype=torch.int64, device=b.device) * _PHI)
+    z = (z ^ _srl(z, 30)) * _M1
+    z = (z ^ _srl(z, 27)) * _M2
+    z = z ^ _srl(z, 31)
+    h = int(z.sum().item()) & ((1 << 64) - 1)
+    parts = [float((h >> (22 * k)) & ((1 << 22) - 1)) for k in range(3)]
+    return torch.tensor([float(r)] + parts, dtype=torch.float64)
+
+
+def check_replicated(digest, group=None) -> bool:
+    """All-gather every rank's replicated_digest; True iff all ranks hold the same r and X bits (the
+    factorisation runs replicated from the all-reduced A: deterministic kernels must give identical bits)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return True
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    d = digest.to(dev)
+    out = [torch.zeros_like(d) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, d, group=group)
+    return all(bool(torch.equal(o, out[0])) for o in out)
+
+
 class CudaBackend:
     """The C-ABI path (binding.Handle) + torch.distributed (NCCL) for the exchange."""
 

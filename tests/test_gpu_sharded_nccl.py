@@ -56,3 +56,21 @@ def test_sharded_single_rank_equals_geninv(H, comm, m, n, r, trans, emulate):
     assert R.in_Q()
     assert C.rel_fro(Gp.cpu().numpy(), R.Gp) <= 1e-9
     assert C.rel_fro(Gp.cpu().numpy(), whole.cpu().numpy()) <= 1e-12
+
+
+def test_sharded_local_failure_returns_everywhere(H, comm):
+    # a rank whose local checks fail still takes part in the pre-check all-reduce and returns the status
+    # (with several ranks the others return it too instead of blocking in the all-reduce of A)
+    from paper_0804_4809_b200.binding import _Info, _opts
+    import ctypes
+    G = torch.zeros(100, 40, dtype=torch.float64, device="cuda")
+    Gp = torch.zeros(40, 100, dtype=torch.float64, device="cuda")
+    rank, info, o = ctypes.c_int64(), _Info(), _opts()
+    st = H._lib.geninv_sharded_d(H._h, ctypes.c_void_p(comm), G.data_ptr(), 100, 40, 40, 0, Gp.data_ptr(), 99,
+                                 ctypes.byref(rank), ctypes.byref(o), ctypes.byref(info))
+    assert st == 1                                           # GENINV_EINVAL: ldp < m_local
+    # the communicator is still usable afterwards: a valid call succeeds
+    G = I.low_rank(7400, 3000, 400, 300).cuda()
+    Gp = torch.empty(400, 3000, dtype=torch.float64, device="cuda")
+    _, sinfo = H.geninv_sharded_d(comm, G, 0, Gp)
+    assert sinfo.rank == 300

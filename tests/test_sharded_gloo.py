@@ -154,3 +154,79 @@ def test_oracle_split_equals_whole():
     G = I.low_rank(22, 300, 90, 60).numpy()
     X, ch = O.from_gram(O.gram(G)[0])
     assert np.array_equal(O.apply(X, G), O.geninv(G).Gp)
+
+
+# ---------------------------------------------------------------- C5 batch split
+def _batch_worker(rank, world, port, nb, q):
+    from oracle import geninv_oracle as O
+    from paper_0804_4809_b200.sharded import batch_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b0, b1 = batch_range(nb, world, rank)
+    Gb = I.make_batch(I.CONFIGS["C5"], 1, b0, b1 - b0).numpy()   # each rank builds only its own matrices
+    Gp, r, _, _ = O.geninv_batched(Gb)                           # independent matrices: no exchange
+    parts = [None] * world
+    dist.all_gather_object(parts, (b0, b1, Gp, r))
+    if rank == 0:
+        q.put(parts)
+    dist.destroy_process_group()
+
+
+def test_batch_split_matches_unsharded():
+    from oracle import geninv_oracle as O
+    nb, world = 37, 2                                # ragged split: 18 + 19 matrices
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_batch_worker, args=(k, world, port, nb, q)) for k in range(world)]
+    for p in ps:
+        p.start()
+    parts = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    Gb = I.make_batch(I.CONFIGS["C5"], 1, 0, nb).numpy()
+    Gp, r, _, _ = O.geninv_batched(Gb)
+    got = np.zeros_like(Gp)
+    rk = np.zeros_like(r)
+    covered = 0
+    for b0, b1, gp, rr in parts:
+        got[b0:b1], rk[b0:b1] = gp, rr
+        covered += b1 - b0
+    assert covered == nb and [p[0] for p in parts] == [0, nb // world]
+    assert np.array_equal(rk, r)
+    assert np.abs(got - Gp).max() <= 1e-13 * np.abs(Gp).max()
+
+
+# ---------------------------------------------------------------- the cross-rank replication check
+def _digest_worker(rank, world, port, perturb, q):
+    from oracle import geninv_oracle as O
+    from paper_0804_4809_b200.sharded import check_replicated, replicated_digest
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    G = I.low_rank(21, 300, 60, 40).numpy()
+    X, ch = O.from_gram(O.gram(G)[0])
+    X = torch.from_numpy(X)
+    if perturb and rank == 1:                        # one flipped low bit on one rank
+        X[7, 3] = torch.nextafter(X[7, 3], torch.tensor(1e300, dtype=torch.float64))
+    ok = check_replicated(replicated_digest(X, ch.rank))
+    if rank == 0:
+        q.put(ok)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("perturb", [False, True])
+def test_check_replicated(perturb):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_digest_worker, args=(k, 2, port, perturb, q)) for k in range(2)]
+    for p in ps:
+        p.start()
+    ok = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok == (not perturb)
