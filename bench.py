@@ -192,6 +192,15 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
+def allsum(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
 def allmax(x: float, world: int) -> float:
     if world == 1:
         return x
@@ -499,19 +508,20 @@ def main():
     # phases (one untimed pass of the split form, CUDA events between the stages; N > 1: torch's all-reduce)
     phases = None
     try:
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        A.zero_()
-        torch.cuda.synchronize()
-        evs[0].record(stream)
-        h.geninv_gram_d(G, trans, A)
-        if world > 1:
-            dist.all_reduce(A)
-        evs[1].record(stream)
-        h.geninv_from_gram_d(A)
-        evs[2].record(stream)
-        h.geninv_apply_d(G, trans, Gp)
-        evs[3].record(stream)
-        torch.cuda.synchronize()
+        for _ in range(2):                           # the first pass captures the chain's CUDA graphs
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            A.zero_()
+            torch.cuda.synchronize()
+            evs[0].record(stream)
+            h.geninv_gram_d(G, trans, A)
+            if world > 1:
+                dist.all_reduce(A)
+            evs[1].record(stream)
+            h.geninv_from_gram_d(A)
+            evs[2].record(stream)
+            h.geninv_apply_d(G, trans, Gp)
+            evs[3].record(stream)
+            torch.cuda.synchronize()
         phases = dict(zip(["gram_allreduce_ms", "factor_inverse_x_ms", "output_ms"],
                           [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(3)]))
     except Exception as exc:
@@ -647,8 +657,9 @@ def bench_batched(args, cfg, desc, world, rank):
     from paper_0804_4809_b200.binding import Handle
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local)
-    nb = cfg.batch // world
-    b0 = rank * nb
+    from paper_0804_4809_b200.sharded import batch_range
+    b0, b1 = batch_range(cfg.batch, world, rank)    # independent matrices: no exchange
+    nb = b1 - b0
     G = I.make_batch(cfg, seed_of(cfg), b0, nb, device=dev)
     Gp = torch.empty(nb, cfg.n, cfg.m, dtype=torch.float64, device=dev)
     rk = torch.empty(nb, dtype=torch.int32, device=dev)
@@ -668,7 +679,7 @@ def bench_batched(args, cfg, desc, world, rank):
     ms = allmax(e0.elapsed_time(e1) / args.steps, world)
     s, ell = min(cfg.m, cfg.n), max(cfg.m, cfg.n)
     ranks = rk.cpu().numpy()
-    F = sum(f_alg(s, ell, np.arange(int(r)))["total"] for r in ranks) * world
+    F = allsum(sum(f_alg(s, ell, np.arange(int(r)))["total"] for r in ranks), world)
     peak, src = fp64_peak()
     value = F / (ms * 1e-3) / 1e9
     # e2e: every step copies this rank's G from pinned host memory, runs geninv_batched_d and reads G+ and
@@ -707,8 +718,8 @@ def bench_batched(args, cfg, desc, world, rank):
         h.use_stream(stream)
         ems = allmax(a0.elapsed_time(a1) / args.steps, world)
         e2e = {"value": F / (ems * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ems,
-               "h2d_bytes_per_step": int(Gh.numel() * 8) * world,
-               "d2h_bytes_per_step": int(Gph.numel() * 8 + rkh.numel() * 4) * world,
+               "h2d_bytes_per_step": int(allsum(Gh.numel() * 8, world)),
+               "d2h_bytes_per_step": int(allsum(Gph.numel() * 8 + rkh.numel() * 4, world)),
                "api": "geninv_batched_d on 8 batch chunks over 3 streams, pinned host G / G+ / rank copies"}
         del Gh, Gph, rkh
     cpu = None

@@ -241,15 +241,34 @@ geninv_status gram_emulated(geninv_handle h, const double *G, long long m, long 
   GI_TRYS(grow(h->emu_sc, h->emu_sc_n, (size_t)emu_scratch_elems((int)s, (int)s)));
   if (!h->emu_flag) GI_TRY(cudaMalloc(&h->emu_flag, sizeof(int)));
   GI_TRY(cudaMemsetAsync(h->emu_flag, 0, sizeof(int), h->st));
-  for (long long k0 = 0; k0 < ell; k0 += KC) {
+  // two-level FP64 accumulation of the exact chunk sums: groups of GRP chunks are summed into the handle's
+  // s x s scratch T, and the group sums into A (a sequential sum over 2^21 / 4096 = 512 chunks would be the
+  // emulated Gram's only rounding; C4: ~sqrt(512) -> ~sqrt(16) + sqrt(32) chunk-sum roundings)
+  constexpr int GRP = 16;
+  const long long nchunks = (ell + KC - 1) / KC;
+  const bool grouped = nchunks > GRP && !accumulate && s <= h->ld;
+  for (long long c = 0; c < nchunks; ++c) {
+    const long long k0 = c * KC;
     const int kc = (int)std::min<long long>(KC, ell - k0);
     if (!trans)
       GI_TRY(emu_split_cols(G + k0 * ld, ld, kc, (int)s, S, h->emu_g, h->emu_eg, h->emu_cm, h->emu_flag, h->st));
     else
       GI_TRY(emu_split(G + k0, ld, (int)s, kc, S, h->emu_g, h->emu_eg, h->emu_flag, h->st));
-    GI_TRY(emu_gemm_nt(h->emu_g, h->emu_eg, (int)s, h->emu_g, h->emu_eg, (int)s, kc, S, T, A, lda, h->emu_sc, h->st,
-                       1, (k0 > 0 || accumulate) ? 1 : 0));
     h->launches += trans ? 2 : 3;
+    if (!grouped) {
+      GI_TRY(emu_gemm_nt(h->emu_g, h->emu_eg, (int)s, h->emu_g, h->emu_eg, (int)s, kc, S, T, A, lda, h->emu_sc, h->st,
+                         1, (k0 > 0 || accumulate) ? 1 : 0));
+      continue;
+    }
+    const bool first_of_group = c % GRP == 0, last_of_group = c % GRP == GRP - 1 || c == nchunks - 1;
+    double *dst = c < GRP ? A : h->T;                      // the first group directly into A
+    const long long ldd = c < GRP ? lda : h->ld;
+    GI_TRY(emu_gemm_nt(h->emu_g, h->emu_eg, (int)s, h->emu_g, h->emu_eg, (int)s, kc, S, T, dst, ldd, h->emu_sc, h->st,
+                       1, first_of_group ? 0 : 1));
+    if (c >= GRP && last_of_group) {   // A += T (lower triangle, in place)
+      GI_TRY(splitk_reduce(h->T, 0, 1, h->ld, A, lda, A, lda, 1.0, (int)s, (int)s, true, h->st));
+      h->launches += 1;
+    }
   }
   int flag = 0;
   GI_TRY(cudaMemcpyAsync(&flag, h->emu_flag, sizeof(int), cudaMemcpyDeviceToHost, h->st));
