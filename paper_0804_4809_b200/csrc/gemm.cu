@@ -98,6 +98,17 @@ static cudaError_t make_map_mn4d(CUtensorMap *map, const Mat &m, int strips) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Bytes of A rows one raster band keeps L2-resident while N sweeps (GENINV_BAND_MB; default 48 MB of the
+// 126 MB L2).
+static long long band_bytes() {
+  static const long long b = [] {
+    const char *e = getenv("GENINV_BAND_MB");
+    const long long mb = e ? atoll(e) : 48;
+    return (mb > 0 ? mb : 48) << 20;
+  }();
+  return b;
+}
+
 template <int BM, int BN, int WM, int WN, int ST, bool AK, bool BK_, bool CHUNK = false>
 static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, WM, WN, ST, AK, BK_>;
@@ -113,9 +124,9 @@ static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
   a.mtiles = (op.M + BM - 1) / BM;
   a.ntiles = (op.N + BN - 1) / BN;
   {
-    // raster band: at most ~48 MB of A rows (BM x K doubles per M-tile) per band, bands balanced
+    // raster band: at most ~band_bytes() of A rows (BM x K doubles per M-tile) per band, bands balanced
     const long long per_tile = (long long)BM * (op.K > 0 ? op.K : 1) * 8;
-    long long mb = std::max<long long>(1, (48LL << 20) / per_tile);
+    long long mb = std::max<long long>(1, band_bytes() / per_tile);
     const long long nb = (a.mtiles + mb - 1) / mb;
     a.mband = (int)((a.mtiles + nb - 1) / nb);
   }
@@ -153,7 +164,7 @@ static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
   std::vector<int> len;
   // tile order of the kernel (lower: row-major over the lower triangle; else the banded raster)
   const long long per_tile = 128LL * (op.K > 0 ? op.K : 1) * 8;
-  const long long mbw = std::max<long long>(1, (48LL << 20) / per_tile);
+  const long long mbw = std::max<long long>(1, band_bytes() / per_tile);
   const long long nbands = (mt + mbw - 1) / mbw;
   const int mband = (int)((mt + nbands - 1) / nbands);
   const double kpm = (double)op.K / op.M;   // pivots evenly spread: piv[j] ~ j K / M (L'L), #{piv < m} ~ m K / M (L M)
