@@ -137,45 +137,68 @@ static cudaError_t launch(const GemmOp &op, GemmArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Split count (1..max_splits) for a 128 x 128 launch that minimises its simulated duration: the
-// tiles x splits CTAs in launch order, each placed on the SM that frees first (one CTA per SM),
-// cost = per-CTA overhead + its k-slabs, plus the fixed-order reduction's traffic.  Per-tile
-// k-ranges follow GemmArgs (device-side pivots assumed evenly spread, rows ~ j * rows / K).
-static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms);
+// Tile size (128 x 128, or 64 x 64 for small products) and split count (1..max_splits) of one chain GEMM that
+// minimise its simulated duration: the tiles x splits CTAs in launch order, each placed on the SM slot that
+// frees first, cost = per-CTA overhead + its k-slabs (a 64 x 64 slab is a quarter of a 128 x 128 one; two
+// 64 x 64 CTAs share an SM), plus the fixed-order reduction's traffic.  Per-tile k-ranges follow GemmArgs
+// (device-side pivots assumed evenly spread, rows ~ j * rows / K).
+static double plan_sim(const GemmOp &op, int S, int tb, int sms);
 
-int balanced_splits(const GemmOp &op, int max_splits, int sms) {
-  if (op.M <= 0 || op.N <= 0 || op.batch < 1 || op.K_dev) return 1;
+static bool small_tiles_allowed() {
+  static const bool on = [] {
+    const char *e = getenv("GENINV_SMALL_TILES");   // 0: 128 x 128 tiles only (A/B measurements)
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+GemmPlan balanced_plan(const GemmOp &op, int max_splits, int sms) {
+  GemmPlan pl;
+  if (op.M <= 0 || op.N <= 0 || op.batch < 1 || op.K_dev) return pl;
   // memoised per shape (the simulation is ~1e4 heap operations; it must not sit on the host path)
   static std::mutex mu;
-  static std::map<std::array<long long, 10>, int> cache;
-  const std::array<long long, 10> key = {op.M, op.N, op.K, op.lower, op.mirror, op.k_lo_mode, op.k_hi_mode, max_splits,
-                                         sms, op.batch};
+  static std::map<std::array<long long, 11>, GemmPlan> cache;
+  const std::array<long long, 11> key = {op.M, op.N, op.K, op.lower, op.mirror, op.k_lo_mode, op.k_hi_mode, max_splits,
+                                         sms, op.batch, small_tiles_allowed()};
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const int S = balanced_splits_sim(op, max_splits, sms);
-  cache[key] = S;
-  return S;
+  double best = 1e300;
+  for (int tb : {128, 64}) {
+    if (tb == 64 && !small_tiles_allowed()) continue;
+    for (int S = 1; S <= max_splits; ++S) {
+      const double t = plan_sim(op, S, tb, sms);
+      if (t < best * 0.97) {   // a split (or the smaller tile) must win by 3 %
+        best = t;
+        pl.splits = S;
+        pl.tile = tb == 64 ? TILE_64x64 : TILE_128x128;
+      }
+    }
+  }
+  cache[key] = pl;
+  return pl;
 }
 
-static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
-  const int mt = (op.M + 127) / 128, nt = (op.N + 127) / 128;
+int balanced_splits(const GemmOp &op, int max_splits, int sms) { return balanced_plan(op, max_splits, sms).splits; }
+
+static double plan_sim(const GemmOp &op, int S, int tb, int sms) {
+  const int mt = (op.M + tb - 1) / tb, nt = (op.N + tb - 1) / tb;
   const long long nsl = (op.K + BK - 1) / BK;
   std::vector<int> len;
   // tile order of the kernel (lower: row-major over the lower triangle; else the banded raster)
-  const long long per_tile = 128LL * (op.K > 0 ? op.K : 1) * 8;
+  const long long per_tile = (long long)tb * (op.K > 0 ? op.K : 1) * 8;
   const long long mbw = std::max<long long>(1, band_bytes() / per_tile);
   const long long nbands = (mt + mbw - 1) / mbw;
   const int mband = (int)((mt + nbands - 1) / nbands);
   const double kpm = (double)op.K / op.M;   // pivots evenly spread: piv[j] ~ j K / M (L'L), #{piv < m} ~ m K / M (L M)
   auto tile_len = [&](int tm, int tn) {
-    const long long m0 = 128LL * tm, n0 = 128LL * tn;
+    const long long m0 = (long long)tb * tm, n0 = (long long)tb * tn;
     long long klo = 0, khi = nsl;
     if (op.k_lo_mode == 1) klo = m0 / BK;
     else if (op.k_lo_mode == 2) klo = n0 / BK;
     else if (op.k_lo_mode == 3) klo = (long long)(m0 * kpm) / BK;
-    if (op.k_hi_mode == 1) khi = std::min(khi, (m0 + 128 + BK - 1) / BK);
-    if (op.k_hi_mode == 2) khi = std::min(khi, ((long long)((m0 + 128) * kpm) + BK - 1) / BK);
+    if (op.k_hi_mode == 1) khi = std::min(khi, (m0 + tb + BK - 1) / BK);
+    if (op.k_hi_mode == 2) khi = std::min(khi, ((long long)((m0 + tb) * kpm) + BK - 1) / BK);
     return (int)std::max(0LL, khi - std::min(klo, khi));
   };
   if (op.lower) {
@@ -190,37 +213,31 @@ static int balanced_splits_sim(const GemmOp &op, int max_splits, int sms) {
       for (int t = 0; t < mb * nt; ++t) len.push_back(tile_len(band * mband + t % mb, t / mb));
     }
   }
-  const double over = 1.0;                              // per-CTA prologue + epilogue, in k-slab units
+  // in 128 x 128 k-slab units (~2.1 us): a 64 x 64 slab is 1/4 of the DMMA work, two such CTAs per SM
+  // each at half the SM's rate -> 1/2 per slab on one of 2 x sms slots; the per-CTA overhead is the same
+  const double over = 1.0, slab = tb == 64 ? 0.5 : 1.0;
+  const int slots = tb == 64 ? 2 * sms : sms;
   static const double red_bw = [] {                      // bytes/s the reduction streams at (tuning override)
     const char *v = getenv("GENINV_RED_GBS");
     return (v ? atof(v) : 3000.0) * 1e9;
   }();
   const double red_per_elem = 8.0 / red_bw / 2.1e-6;     // slab units per element of the reduction
   const double out_elems = op.lower ? 0.5 * op.M * (op.M + 1.0) : (double)op.M * op.N;   // lower: partials lower only
-  double best = 1e300;
-  int bs = 1;
-  for (int S = 1; S <= max_splits; ++S) {
-    std::priority_queue<double, std::vector<double>, std::greater<double>> q;
-    for (int i = 0; i < sms; ++i) q.push(0.0);
-    double span = 0.0;
-    for (int b = 0; b < op.batch; ++b)
+  std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+  for (int i = 0; i < slots; ++i) q.push(0.0);
+  double span = 0.0;
+  for (int b = 0; b < op.batch; ++b)
     for (int z = 0; z < S; ++z)
       for (int l : len) {
         const int per = (l + S - 1) / S;
         const int mine = std::max(0, std::min(l, per * (z + 1)) - std::min(l, per * z));
         const double t0 = q.top();
         q.pop();
-        const double t1 = t0 + over + mine;
+        const double t1 = t0 + over + slab * mine;
         q.push(t1);
         span = std::max(span, t1);
       }
-    const double total = span + (S > 1 ? (S + 1.0) * out_elems * op.batch * red_per_elem + 2.0 : 0.0);
-    if (total < best * 0.97) {   // a split must win by 3 %
-      best = total;
-      bs = S;
-    }
-  }
-  return bs;
+  return span + (S > 1 ? (S + 1.0) * out_elems * op.batch * red_per_elem + 2.0 : 0.0);
 }
 
 int upd_tile_bm() {
@@ -265,6 +282,12 @@ cudaError_t gemm(const GemmOp &op, cudaStream_t st) {
     if (op.a_kmajor && !op.b_kmajor) return launch<128, 32, 32, 32, 6, true, false>(op, a, st);
     if (!op.a_kmajor && op.b_kmajor) return launch<128, 32, 32, 32, 6, false, true>(op, a, st);
     return launch<128, 32, 32, 32, 6, false, false>(op, a, st);
+  }
+  if (op.tile == TILE_64x64) {   // small chain products (balanced_plan): 4 warps of 32 x 32, 4 stages
+    if (op.a_kmajor && op.b_kmajor) return launch<64, 64, 32, 32, 4, true, true>(op, a, st);
+    if (op.a_kmajor && !op.b_kmajor) return launch<64, 64, 32, 32, 4, true, false>(op, a, st);
+    if (!op.a_kmajor && op.b_kmajor) return launch<64, 64, 32, 32, 4, false, true>(op, a, st);
+    return launch<64, 64, 32, 32, 4, false, false>(op, a, st);
   }
   if (op.a_kmajor && op.b_kmajor) return launch<128, 128, 64, 32, 6, true, true>(op, a, st);
   if (op.a_kmajor && !op.b_kmajor) return launch<128, 128, 64, 32, 6, true, false>(op, a, st);

@@ -12,7 +12,7 @@ struct Mat {               // row-major device matrix (or batch of equally-shape
   long long bstride = 0;   // elements between batch items
 };
 
-enum Tile { TILE_128x128 = 0, TILE_128x32 = 1 };   // TILE_128x32: N = 32 panel updates (256 x 32 when both operands are K-major, see upd_tile_bm)
+enum Tile { TILE_128x128 = 0, TILE_128x32 = 1, TILE_64x64 = 2 };   // TILE_128x32: N = 32 panel updates (256 x 32 when both operands are K-major, see upd_tile_bm)
 
 struct GemmOp {
   Mat A;  bool a_kmajor = true;  int a_mn0 = 0, a_k0 = 0;
@@ -49,7 +49,12 @@ int num_sms();   // SM count of the current device (cached per device)
 // context: done once per (kernel, device), thread-safe).
 cudaError_t smem_optin(const void *fn, int bytes);
 
-// Split-K count for a 128 x 128 launch from a schedule simulation (see gemm.cu); 1 = no split.
-int balanced_splits(const GemmOp &op, int max_splits, int sms);
+// Tile size and split-K count of a chain product from a schedule simulation (see gemm.cu).
+struct GemmPlan {
+  int splits = 1;
+  Tile tile = TILE_128x128;
+};
+GemmPlan balanced_plan(const GemmOp &op, int max_splits, int sms);
+int balanced_splits(const GemmOp &op, int max_splits, int sms);   // balanced_plan(...).splits
 
 }  // namespace gi

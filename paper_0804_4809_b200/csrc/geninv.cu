@@ -525,18 +525,22 @@ GemmOp op_x(geninv_handle h, int s, int r) {   // X = K K' (s x s, full symmetri
   return x;
 }
 
-int chain_splits(const GemmOp &op) {
+// Tile size (128 x 128 or 64 x 64) and split-K count of one chain GEMM (balanced_plan's simulation).
+GemmPlan chain_plan(const GemmOp &op) {
   static const int on = [] {
     const char *e = getenv("GENINV_CHAIN_SPLIT");   // 0 disables (tuning / A-B runs)
     return e ? atoi(e) : 1;
   }();
-  return on ? balanced_splits(op, 8, num_sms()) : 1;
+  return on ? balanced_plan(op, 8, num_sms()) : GemmPlan();
 }
+int chain_splits(const GemmOp &op) { return chain_plan(op).splits; }
 
 // One chain GEMM with the split-K count of its schedule simulation; partial slices in h->part
 // (sized by prepare_chain beforehand: no allocation while a graph is being captured).
 geninv_status gemm_chain(geninv_handle h, GemmOp op) {
-  int S = chain_splits(op);
+  const GemmPlan pl = chain_plan(op);
+  int S = pl.splits;
+  op.tile = pl.tile;
   const long long pstride = (long long)op.M * op.N;
   while (S > 1 && (size_t)S * pstride * sizeof(double) > h->part_bytes) --S;
   if (getenv("GENINV_DEBUG_SPLITS"))

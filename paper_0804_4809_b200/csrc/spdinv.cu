@@ -104,13 +104,14 @@ std::vector<GemmOp> trtri_ops(double *C, long long ldc, int r, double *Ci, long 
   return ops;
 }
 
-int trtri_splits(const GemmOp &op) {
+GemmPlan trtri_plan(const GemmOp &op) {
   static const int on = [] {
     const char *e = getenv("GENINV_CHAIN_SPLIT");
     return e ? atoi(e) : 1;
   }();
-  return on ? balanced_splits(op, 8, num_sms()) : 1;
+  return on ? balanced_plan(op, 8, num_sms()) : GemmPlan();
 }
+int trtri_splits(const GemmOp &op) { return trtri_plan(op).splits; }
 
 int trtri_launches(int r, long long ldc, long long ldi, long long part_elems) {
   const int r_pad = (r + 31) / 32 * 32;
@@ -159,7 +160,9 @@ cudaError_t trtri_lower(double *C, long long ldc, int r, double *Ci, long long l
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   for (GemmOp op : trtri_ops(C, ldc, r, Ci, ldi, T)) {
-    int S = part ? trtri_splits(op) : 1;
+    const GemmPlan pl = trtri_plan(op);
+    op.tile = pl.tile;
+    int S = part ? pl.splits : 1;
     const long long per = (long long)op.M * op.N;
     while (S > 1 && (long long)S * op.batch * per > part_elems) --S;
     if (S <= 1) {
