@@ -57,6 +57,26 @@ def test_gram_integer_bit_exact(H, shape):
     assert np.array_equal(got[low], Ao[low])
 
 
+@pytest.mark.parametrize("shape", [(1 << 18, 200), (200, 1 << 18), (300000, 130)])
+def test_gram_two_level_integer_bit_exact(H, shape):
+    # long sums: each CTA's k-range exceeds the 8192-row register chunk, so the CHUNK instance of the
+    # Gram runs (chunk sums added into the tile in memory, then the pairwise split-K reduction); with
+    # integer entries every partial sum is exact, so the result must be the exact Gram bit for bit (P1)
+    rng = np.random.default_rng(shape[0] + shape[1])
+    G = rng.integers(-3, 4, size=shape).astype(float)
+    m, n = shape
+    tr = int(m < n)
+    s = min(m, n)
+    A = torch.full((s, (s + 1) // 2 * 2), np.nan, dtype=torch.float64, device="cuda")
+    H.geninv_gram_d(padded(G, n), tr, A)
+    torch.cuda.synchronize()
+    # the exact Gram: integer entries, |every partial sum| <= 9 * 300000 < 2^53, so any FP64 summation order
+    # (here the host BLAS) is exact
+    Ao = (G @ G.T) if tr else (G.T @ G)
+    low = np.tril_indices(s)
+    assert np.array_equal(A[:, :s].cpu().numpy()[low], Ao[low])
+
+
 @pytest.mark.parametrize("shape", [(3000, 257), (257, 3000)])
 def test_gram_random(H, shape):
     G = I.dense_normal(3, *shape).numpy()

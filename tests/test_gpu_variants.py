@@ -1,5 +1,6 @@
 """Schedule variants of the factorisation chain (`-m gpu`): the lookahead depth (1, 2, 3), one or
-two update streams, CUDA graphs on/off and the chain GEMMs' split-K on/off change only the order
+two update streams, CUDA graphs on/off, the chain GEMMs' split-K on/off, their 64 x 64 tiles on/off and
+the Gram's register-chunk length (one chunk; 512 rows, i.e. a flush every 32 k-slabs) change only the order
 in which partial sums are added, never a decision.  Each variant runs in its own
 process (the knobs are read once per process) on the same seeded inputs; rank and pivots must be
 identical to the default schedule, G+ within the summation-order noise (1e-10 relative, an order below
@@ -48,12 +49,17 @@ VARIANTS = {
     "no_graph": {"GENINV_NO_GRAPH": "1"},
     "no_chain_split": {"GENINV_CHAIN_SPLIT": "0"},
     "upd_tile_128": {"GENINV_UPD_TILE_BM": "128"},
+    "no_small_tiles": {"GENINV_SMALL_TILES": "0"},
+    "gram_one_chunk": {"GENINV_GRAM_CHUNK_ROWS": "0"},
+    "gram_chunk_512": {"GENINV_GRAM_CHUNK_ROWS": "512"},
+    "trtri_levels_only": {"GENINV_CHAIN_SPLIT": "0", "GENINV_SMALL_TILES": "0"},
 }
 
 
 def run_variant(tmp_path, name, env_extra):
     env = dict(os.environ)
-    for k in ("GENINV_LOOKAHEAD", "GENINV_ONE_UPD_STREAM", "GENINV_NO_GRAPH", "GENINV_CHAIN_SPLIT", "GENINV_UPD_TILE_BM"):
+    for k in ("GENINV_LOOKAHEAD", "GENINV_ONE_UPD_STREAM", "GENINV_NO_GRAPH", "GENINV_CHAIN_SPLIT", "GENINV_UPD_TILE_BM",
+              "GENINV_SMALL_TILES", "GENINV_GRAM_CHUNK_ROWS"):
         env.pop(k, None)
     env.update(env_extra)
     prefix = str(tmp_path / name)
