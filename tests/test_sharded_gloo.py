@@ -230,3 +230,48 @@ def test_check_replicated(perturb):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert ok == (not perturb)
+
+
+# ---------------------------------------------------------------- consistency across P
+def _p_worker(rank, world, port, m, n, r, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    G = I.low_rank(seed, m, n, r)
+    r0, r1 = row_range(m, world, rank)
+    A = torch.zeros(n, n, dtype=torch.float64)
+    Gp = torch.zeros(n, r1 - r0, dtype=torch.float64)
+    be = OracleBackend(0)
+    res = sharded_geninv(be, G[r0:r1].contiguous(), A, Gp)
+    blocks = [None] * world
+    dist.all_gather_object(blocks, (r0, r1, Gp.numpy(), res.rank, res.info.piv.tolist()))
+    if rank == 0:
+        q.put(blocks)
+    dist.destroy_process_group()
+
+
+def test_consistency_across_P():
+    # the grouping of the Gram's partial sums changes with P; under Q the decisions (r, piv) must not, and
+    # G+ stays within rounding ("identical r and piv, G+ within ~1e-11")
+    from oracle import checks as C
+    from oracle import geninv_oracle as O
+    m, n, r, seed = 900, 120, 80, 21
+    G = I.low_rank(seed, m, n, r).numpy()
+    R = O.geninv(G)
+    assert R.in_Q()
+    ctx = mp.get_context("spawn")
+    for world in (2, 3):
+        q = ctx.Queue()
+        port = _free_port()
+        ps = [ctx.Process(target=_p_worker, args=(k, world, port, m, n, r, seed, q)) for k in range(world)]
+        for p in ps:
+            p.start()
+        blocks = q.get(timeout=180)
+        for p in ps:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        Gp = np.zeros((n, m))
+        for r0, r1, blk, rk, piv in blocks:
+            assert rk == R.rank == r and piv == R.piv.tolist()
+            Gp[:, r0:r1] = blk
+        assert C.rel_fro(Gp, R.Gp) <= 1e-11, world
