@@ -85,7 +85,10 @@ typedef struct {
   double min_pivot;  /* smallest c_k over all columns */
   int32_t order;     /* a7 product order used by geninv_d: 0 = X G' / G' X with X = K K';
                         1 = K (K' G') / (G' K) K' (low rank) */
-  int32_t reserved;
+  int32_t not_psd_hint; /* 1 if a tentative pivot fell below -s * tol (SPEC's definiteness rule): the
+                           paper drops it like any pivot <= tol, so it is not an error -- G'G never
+                           produces one beyond rounding, a user-supplied non-PSD A (geninv_from_gram_d,
+                           geninv_frchol_d) does */
 } geninv_info;
 
 typedef struct geninv_handle_s *geninv_handle;

@@ -35,7 +35,7 @@ class _Opts(ctypes.Structure):
 class _Info(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("rank", ctypes.c_int64), ("transposed", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("min_acc", ctypes.c_double), ("max_drop", ctypes.c_double),
-                ("min_pivot", ctypes.c_double), ("order", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("min_pivot", ctypes.c_double), ("order", ctypes.c_int32), ("not_psd_hint", ctypes.c_int32)]
 
 
 @dataclass
@@ -48,6 +48,7 @@ class Info:
     max_drop: float
     min_pivot: float
     order: int = 0       # a7 product order of geninv_d: 0 = X G', 1 = K (K' G') (low rank, f4)
+    not_psd_hint: int = 0  # a tentative pivot below -s * tol (user-supplied A not PSD; reported, not an error)
 
     @property
     def mu_acc(self):
@@ -301,4 +302,4 @@ class Handle:
 
 def _info(i: _Info) -> Info:
     return Info(i.tol, int(i.rank), bool(i.transposed), int(i.status), i.min_acc, i.max_drop, i.min_pivot,
-                int(i.order))
+                int(i.order), int(i.not_psd_hint))

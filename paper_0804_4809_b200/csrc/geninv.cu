@@ -788,7 +788,11 @@ geninv_status apply(geninv_handle h, const double *G, long long m, long long n, 
   return GENINV_OK;
 }
 
-void fill_info(geninv_info *info, const FactorStats &fs, int r, int tr, geninv_status st) {
+// s: the factored size (0: unknown).  not_psd_hint: a tentative pivot below -s * tol (SPEC S:138's
+// definiteness rule) -- the paper drops it like any other pivot <= tol (reading R3), so it is
+// reported, not an error: a Gram matrix G'G never produces one beyond rounding, a user-supplied A that is
+// not positive semidefinite does.
+void fill_info(geninv_info *info, const FactorStats &fs, int r, int tr, geninv_status st, long long s = 0) {
   if (!info) return;
   info->tol = fs.tol;
   info->rank = r;
@@ -798,6 +802,7 @@ void fill_info(geninv_info *info, const FactorStats &fs, int r, int tr, geninv_s
   info->max_drop = fs.max_drop;
   info->min_pivot = fs.min_pivot;
   info->order = 0;
+  info->not_psd_hint = (s > 0 && fs.tol > 0 && fs.min_pivot < -(double)s * fs.tol) ? 1 : 0;
 }
 
 geninv_status check_g(const double *G, long long m, long long n, long long ld) {
@@ -988,7 +993,7 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
     FactorStats fs{};
     geninv_status st = small_path(h, G, m, n, ld, Gp, ldp, opts, &r, &fs);
     if (rank) *rank = r;
-    fill_info(info, fs, r, tr, st);
+    fill_info(info, fs, r, tr, st, s);
     return st;
   }
   long long ldg = ld;
@@ -1006,7 +1011,7 @@ geninv_status geninv_d(geninv_handle h, const double *G, int64_t m, int64_t n, i
     if (e != cudaSuccess) st = cuda_status(e);
   }
   if (rank) *rank = r;
-  fill_info(info, fs, r, tr, st);
+  fill_info(info, fs, r, tr, st, s);
   if (info) info->order = ko ? 1 : 0;
   return st;
 }
@@ -1093,7 +1098,7 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
       GI_TRY(cudaStreamSynchronize(h->st));
     }
     if (rank) *rank = r;
-    fill_info(info, fs, r, tr, st);
+    fill_info(info, fs, r, tr, st, s);
     return st;
   }
   const long long ldg = (n + 1) / 2 * 2;  // device copy: even leading dimension
@@ -1142,7 +1147,7 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
   geninv_status st = from_gram(h, h->A, s, h->ld, opts, &r, &fs);
   if (st == GENINV_OK) st = finish_spd_check(h, r);
   if (st != GENINV_OK) {
-    fill_info(info, fs, r, tr, st);
+    fill_info(info, fs, r, tr, st, s);
     return st;
   }
   // ---- output in chunks, D2H of chunk c overlapped with the product of chunk c + 1
@@ -1212,7 +1217,7 @@ geninv_status geninv_host_d(geninv_handle h, const double *G_host, int64_t m, in
   GI_TRY(cudaStreamSynchronize(h->st2));
   GI_TRY(cudaStreamSynchronize(h->st));
   if (rank) *rank = r;
-  fill_info(info, fs, r, tr, GENINV_OK);
+  fill_info(info, fs, r, tr, GENINV_OK, s);
   return GENINV_OK;
 }
 
@@ -1292,7 +1297,7 @@ geninv_status geninv_sharded_d(geninv_handle h, void *nccl_comm, const double *G
     if (e != cudaSuccess) st = cuda_status(e);
   }
   if (rank) *rank = r;
-  fill_info(info, fs, r, trans, st);
+  fill_info(info, fs, r, trans, st, s);
   return st;
 }
 
@@ -1324,7 +1329,7 @@ geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_
   if (st == GENINV_OK) st = finish_spd_check(h, r);
   if (st != GENINV_OK) {
     if (rank) *rank = r;
-    fill_info(info, fs, r, tr, st);
+    fill_info(info, fs, r, tr, st, s);
     return st;
   }
   const long long ldt = (k + 1) / 2 * 2;
@@ -1373,7 +1378,7 @@ geninv_status geninv_solve_d(geninv_handle h, const double *G, int64_t m, int64_
   cudaError_t e = cudaStreamSynchronize(h->st);
   if (e != cudaSuccess) st = cuda_status(e);
   if (rank) *rank = r;
-  fill_info(info, fs, r, tr, st);
+  fill_info(info, fs, r, tr, st, s);
   return st;
 }
 
@@ -1399,7 +1404,7 @@ geninv_status geninv_from_gram_d(geninv_handle h, const double *A, int64_t s, in
   geninv_status st = from_gram(h, A, (int)s, lda, opts, &r, &fs);
   if (st == GENINV_OK) st = finish_spd_check(h, r);
   if (rank) *rank = r;
-  fill_info(info, fs, r, 0, st);
+  fill_info(info, fs, r, 0, st, s);
   return st;
 }
 
@@ -1432,7 +1437,7 @@ geninv_status geninv_frchol_d(geninv_handle h, const double *A, int64_t s, int64
     GI_TRY(cudaStreamSynchronize(h->st));
   }
   if (rank) *rank = r;
-  fill_info(info, fs, r, 0, st);
+  fill_info(info, fs, r, 0, st, s);
   return st;
 }
 

@@ -139,6 +139,9 @@ def test_frchol_margins_golden(H, k):
     assert info.min_pivot == ex["min_pivot"]
     if ex["tol"] is None:
         assert info.tol == ex["tol_expected"]
+    # this A is not PSD: the pivot -7 is far below -s * tol with the paper's tol (reported, not an error);
+    # with tol = 1 the worst dropped pivot -1/2 is within -s * tol
+    assert info.not_psd_hint == (1 if ex["tol"] is None else 0)
 
 
 @pytest.mark.parametrize("r,seed", [(8, 0), (32, 1), (33, 2), (64, 3), (100, 4)])
