@@ -163,3 +163,26 @@ def test_tiny_scale_fails_loudly(H, m, n):
     torch.cuda.synchronize()
     assert int(rk[0]) == -GENINV_ERANGE
     assert torch.isnan(Gp).all()
+
+
+# seeds: first seed >= m * 13 + n with oracle margins in Q (tools/screen_q_cpu.py test_batched_shape_sweep)
+BATCHED_SWEEP_SEED = {(1, 1, 1): 14, (7, 3, 3): 94, (3, 7, 2): 46, (64, 64, 64): 896, (128, 64, 64): 1728,
+                      (64, 128, 64): 960, (100, 63, 41): 1363, (63, 100, 41): 919, (128, 17, 17): 1681,
+                      (17, 128, 9): 349, (96, 64, 40): 1312, (64, 96, 40): 928, (127, 57, 33): 1708,
+                      (57, 127, 56): 868, (120, 8, 5): 1568, (9, 121, 9): 238}
+
+
+@pytest.mark.parametrize("m,n,r", list(BATCHED_SWEEP_SEED))
+def test_batched_shape_sweep(H, m, n, r):
+    # the batched kernel streams G through a ring of chunk buffers (Gram) and through Q (output), and
+    # parks L's fragments in TMEM across the SPD inverse: ragged s / ell, both orientations, full rank
+    G = I.low_rank(BATCHED_SWEEP_SEED[(m, n, r)], m, n, r)
+    R = O.geninv(G.numpy())
+    assert R.in_Q() and R.rank == r
+    Gs = torch.stack([G, torch.zeros(m, n, dtype=torch.float64), 2.0 * G]).cuda()
+    Gp, rk = H.geninv_batched_d(Gs)
+    torch.cuda.synchronize()
+    assert rk.tolist() == [r, 0, r]
+    assert C.rel_fro(Gp[0].cpu().numpy(), R.Gp) <= 1e-9
+    assert bool((Gp[1] == 0).all())
+    assert C.rel_fro(2.0 * Gp[2].cpu().numpy(), R.Gp) <= 1e-9

@@ -22,6 +22,22 @@ __global__ void chain(double x0, double *out, long long *cyc) {
     if (OP == 5) x = rsqrt(x) + 0.5;                               // rsqrt (+ DADD)
     if (OP == 6) x = __drcp_rn(x);                                 // __drcp_rn
     if (OP == 7) x = x * c;                                        // DMUL
+    if (OP == 8) {                                                 // DMMA.8x8x4, accumulator chain
+      double c0 = x, c1 = x;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c0), "+d"(c1) : "d"(c), "d"(e));
+      x = c0;
+    }
+    if (OP == 9) {                                                 // DMMA, then an LDS of the next operand
+      __shared__ double sh[64];
+      sh[threadIdx.x] = x;
+      __syncwarp();
+      double b = sh[(threadIdx.x + 1) & 31];
+      double c0 = 0.0, c1 = 0.0;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c0), "+d"(c1) : "d"(c), "d"(b));
+      x = c0 * 1e-3 + 1.0;
+    }
   }
   long long t1 = clock64();
   out[threadIdx.x] = x;
@@ -50,5 +66,7 @@ int main() {
   run<6>(o, c, "__drcp_rn");
   run<5>(o, c, "rsqrt + dadd");
   run<4>(o, c, "shfl + dmul");
+  run<8>(o, c, "dmma (acc chain)");
+  run<9>(o, c, "sts+lds+dmma+dfma");
   return 0;
 }

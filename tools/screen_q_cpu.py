@@ -38,6 +38,11 @@ CASES = {
     "test_solve_parity": [((m, n, r), m * 7 + n) for (m, n, r) in
                           [(300, 130, 70), (130, 300, 70), (2050, 530, 400), (257, 255, 200), (96, 64, 40),
                            (64, 64, 64)]],
+    # the batched kernel's chunk rings and output chunks: both orientations, ragged s and ell, full rank
+    "test_batched_shape_sweep": [((m, n, r), m * 13 + n) for (m, n, r) in
+                                 [(1, 1, 1), (7, 3, 3), (3, 7, 2), (64, 64, 64), (128, 64, 64), (64, 128, 64),
+                                  (100, 63, 41), (63, 100, 41), (128, 17, 17), (17, 128, 9), (96, 64, 40),
+                                  (64, 96, 40), (127, 57, 33), (57, 127, 56), (120, 8, 5), (9, 121, 9)]],
     "test_sharded": [((m, n, r), m + 11 * n) for (m, n, r) in [(3000, 400, 300), (400, 3000, 300),
                                                                (9000, 3200, 3000)]],
 }
