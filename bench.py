@@ -50,20 +50,31 @@ def seed_of(cfg) -> int:
 
 
 # --------------------------------------------------------------------------- flop model
-def f_alg(s: int, ell: int, piv: np.ndarray) -> dict:
-    """Algorithmic FP64 flops of one geninv (SURVEY §8(a) convention: SYRKs count one triangle)."""
+def fullrank_direct() -> bool:
+    """The library evaluates r = s through L^-1 (DESIGN reading R27) unless GENINV_FULLRANK_DIRECT=0."""
+    return os.environ.get("GENINV_FULLRANK_DIRECT", "1") != "0"
+
+
+def f_alg(s: int, ell: int, piv: np.ndarray, direct: bool = False) -> dict:
+    """Algorithmic FP64 flops of one geninv in the evaluation order that runs (SURVEY §8(a) convention: SYRKs
+    count one triangle).  direct (r = s, R27): X = L^-T L^-1 as one TRTRI (s^3/3) and one LAUUM (s^3/3) in
+    place of L'L, the SPD inverse and K, X."""
     r = len(piv)
     k = np.arange(s)
     rk = np.searchsorted(np.sort(piv), k, side="left")      # columns accepted before column k
     chol = float(np.sum(2.0 * (s - k) * rk + (s - k)))
-    parts = {
-        "gram": float(ell) * s * (s + 1),
-        "chol": chol,
-        "ltl": float(s) * r * (r + 1),
-        "inv": float(r) ** 3,
-        "kx": 2.0 * s * r * r + float(s) * (s + 1) * r,
-        "out": 2.0 * s * s * ell,
-    }
+    if direct and r == s:
+        parts = {"gram": float(ell) * s * (s + 1), "chol": chol, "inv": 2.0 * float(s) ** 3 / 3.0,
+                 "out": 2.0 * s * s * ell}
+    else:
+        parts = {
+            "gram": float(ell) * s * (s + 1),
+            "chol": chol,
+            "ltl": float(s) * r * (r + 1),
+            "inv": float(r) ** 3,
+            "kx": 2.0 * s * r * r + float(s) * (s + 1) * r,
+            "out": 2.0 * s * s * ell,
+        }
     parts["total"] = sum(parts.values())
     return parts
 
@@ -434,7 +445,7 @@ def main():
     _, piv, _ = h.geninv_frchol_d(Aw)
     piv = piv.cpu().numpy()
     del Aw
-    F = f_alg(s, ell, piv)
+    F = f_alg(s, ell, piv, direct=fullrank_direct() and not (s <= 64 and ell <= 128))
     for _ in range(max(0, args.warmup - 1)):
         step()
     # inputs (G and G+) that fit in the 126 MB L2 are flushed between timed steps by writing a 512 MB

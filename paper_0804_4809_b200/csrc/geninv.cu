@@ -617,12 +617,34 @@ __global__ void async_rank_kernel(int64_t *out, const int *rk_final, const Facto
                                             : r;
 }
 
+// Full rank (r = s) evaluated through L^-1 (reading R27); GENINV_FULLRANK_DIRECT=0 forces the general path.
+bool fullrank_direct_on() {
+  static const bool on = [] {
+    const char *e = getenv("GENINV_FULLRANK_DIRECT");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 // a4-a6 after the factorisation: K = L M (s x r) and, if want_x, X (s x s, full) = K K' = L M M L'.
 // rk_pad (device, optional): r is the full size s and the detected rank is *rk_pad (see above).
 geninv_status build_x(geninv_handle h, int s, int r, bool want_x = true, const int *rk_pad = nullptr) {
   const long long ld = h->ld;
   if (r == 0) {
     GI_TRY(cudaMemsetAsync(h->X, 0, (size_t)s * ld * sizeof(double), h->st));
+    return GENINV_OK;
+  }
+  if (r == s && want_x && !rk_pad && fullrank_direct_on()) {
+    // Every column kept: L is square lower triangular with a positive diagonal, so M = inv(L'L) = L^-1 L^-T
+    // exactly, K = L M = L^-T and X = K K' = L^-T L^-1 (P:137-139 with the products collapsed, R27): one
+    // TRTRI of L and one LAUUM instead of L'L, the SPD Cholesky of L'L, its TRTRI and LAUUM, K and X.
+    const int r_pad = (r + 31) / 32 * 32;
+    if (r_pad > s) GI_TRY(cudaMemsetAsync(h->L + (long long)s * ld, 0, (size_t)(r_pad - s) * ld * sizeof(double), h->st));
+    GI_TRY(cudaMemsetAsync(h->Ci, 0, (size_t)r_pad * ld * sizeof(double), h->st));
+    GI_TRY(cudaMemsetAsync(h->fs2, 0, sizeof(FactorStats), h->st));   // no SPD factorisation: no flags
+    GI_TRY(trtri_lower(h->L, ld, r, h->Ci, ld, h->T, h->part, (long long)(h->part_bytes / sizeof(double)), h->st));
+    GI_TRYS(gemm_chain(h, op_lauum(h, r, h->X, ld)));                  // X = Ci' Ci
+    h->launches += 3 + trtri_launches(r, ld, ld, (long long)(h->part_bytes / sizeof(double)));
     return GENINV_OK;
   }
   GI_TRYS(gemm_chain(h, op_ltl(h, s, r)));

@@ -104,6 +104,33 @@ def test_c2_full_rank(H):
     assert max(penrose_gpu(G, Gp)) <= PENROSE
 
 
+_GENERAL_PATH_C2 = r"""
+import numpy as np, torch
+from oracle import checks as C
+from oracle import geninv_oracle as O
+from paper_0804_4809_b200 import inputs as I
+from paper_0804_4809_b200.binding import Handle
+G = I.make_single(I.CONFIGS["C2"], 1).numpy()
+Gp, info = Handle(0).geninv_d(torch.as_tensor(G).cuda())
+assert info.rank == 1024
+e = C.rel_fro(Gp.cpu().numpy(), O.geninv(G).Gp)
+assert e <= 1e-12, e
+print("ok", e)
+"""
+
+
+def test_c2_full_rank_general_path():
+    # r = s runs L^-T L^-1 by default (R27); GENINV_FULLRANK_DIRECT=0 forces the general chain (L'L, its SPD
+    # inverse, K, X) -- same gates (the switch is read once per process, hence the subprocess)
+    import subprocess
+    import sys
+    env = dict(os.environ, GENINV_FULLRANK_DIRECT="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", _GENERAL_PATH_C2], env=env, cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
+
+
 def test_zero_and_nonfinite(H):
     from paper_0804_4809_b200.binding import GeninvError, GENINV_ENONFINITE
     Gp, info = run(H, np.zeros((40, 30)))
