@@ -104,6 +104,27 @@ def test_c2_full_rank(H):
     assert max(penrose_gpu(G, Gp)) <= PENROSE
 
 
+# seeds: first seed >= m * 5 + n with oracle margins in Q (tools/screen_q_cpu.py test_full_rank_direct)
+# (a square random G has mu_acc ~1e4 -- the edge of Q where R23 says no FP64 evaluation is determined to 1e-9 --
+#  so the fifth case is mildly tall)
+FULL_RANK_SEED = {(700, 333, 333): 3833, (333, 700, 333): 2365, (2050, 97, 97): 10347, (97, 2050, 97): 2535,
+                  (420, 300, 300): 2400}
+
+
+@pytest.mark.parametrize("m,n,r", list(FULL_RANK_SEED))
+def test_full_rank_direct(H, m, n, r):
+    # r = s through X = L^-T L^-1 (R27): s not a multiple of 32 (TRTRI pads L with an identity block), both
+    # orientations; same gates as every other case
+    G = I.low_rank(FULL_RANK_SEED[(m, n, r)], m, n, r).numpy()
+    R = O.geninv(G)
+    assert R.in_Q() and R.rank == r == min(m, n)
+    Gp, info = run(H, G)
+    assert info.rank == r
+    assert C.rel_fro(Gp, R.Gp) <= REL
+    # Penrose: 1e-10 on Q* margins, 1e-9 on Q (as R22); these seeds' mu_acc is 2e5 - 4e6
+    assert max(penrose_gpu(G, Gp)) <= (PENROSE if R.in_Qstar() else 1e-9)
+
+
 _GENERAL_PATH_C2 = r"""
 import numpy as np, torch
 from oracle import checks as C
