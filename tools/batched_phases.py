@@ -27,7 +27,7 @@ def main():
     Gp, rk = h.geninv_batched_d(G, Gp, rk)
     torch.cuda.synchronize()
     lib = B.load()
-    buf = np.zeros((4096, 12), dtype=np.int64)
+    buf = np.zeros((4096, 16), dtype=np.int64)
     lib.geninv_debug_batched_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.geninv_debug_batched_times(buf.ctypes.data, 4096)
     t = buf[:min(nb, 4096)]
@@ -37,6 +37,10 @@ def main():
     print(f"cycles per matrix (median over {len(t)} CTAs): total {np.median(tot):.0f}")
     for name, col in zip(NAMES, d.T):
         print(f"  {name:12s} {np.median(col):8.0f}  ({np.median(col) / np.median(tot) * 100:4.1f} %)")
+    # one sweep step (k0 = 8): chain (V rows), barrier 1, update + K entries + publish, barrier 2
+    if t[:, 12].any():
+        st = np.diff(t[:, [12, 7, 13, 11]], axis=1)
+        print("  sweep step k0 = 8: chain %.0f, barrier %.0f, update/fix/publish %.0f cycles" % tuple(np.median(st, axis=0)))
 
 
 if __name__ == "__main__":
