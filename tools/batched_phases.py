@@ -27,7 +27,7 @@ def main():
     Gp, rk = h.geninv_batched_d(G, Gp, rk)
     torch.cuda.synchronize()
     lib = B.load()
-    buf = np.zeros((4096, 20), dtype=np.int64)
+    buf = np.zeros((4096, 16), dtype=np.int64)
     lib.geninv_debug_batched_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.geninv_debug_batched_times(buf.ctypes.data, 4096)
     t = buf[:min(nb, 4096)]
@@ -42,10 +42,8 @@ def main():
         st = np.diff(t[:, [12, 7, 13, 11]], axis=1)
         print("  sweep step k0 = 8: chain %.0f, barrier %.0f, update/fix/publish %.0f cycles" % tuple(np.median(st, axis=0)))
     if t[:, 14].any():
-        print("  output: start -> chunk 1 ready %.0f, chunk 1 products %.0f, -> end %.0f cycles" % (
-            np.median(t[:, 14] - t[:, 9]), np.median(t[:, 15] - t[:, 14]), np.median(t[:, 10] - t[:, 15])))
-        print("  output: start -> chunk 0 ready %.0f, chunk 0 products %.0f, -> chunk 1 ready %.0f cycles" % (
-            np.median(t[:, 16] - t[:, 9]), np.median(t[:, 17] - t[:, 16]), np.median(t[:, 14] - t[:, 17])))
+        print("  output: start -> chunk 0 ready %.0f, chunk 0 products %.0f cycles" % (
+            np.median(t[:, 14] - t[:, 9]), np.median(t[:, 15] - t[:, 14])))
 
 
 if __name__ == "__main__":
