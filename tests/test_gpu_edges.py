@@ -169,13 +169,14 @@ def test_tiny_scale_fails_loudly(H, m, n):
 BATCHED_SWEEP_SEED = {(1, 1, 1): 14, (7, 3, 3): 94, (3, 7, 2): 46, (64, 64, 64): 896, (128, 64, 64): 1728,
                       (64, 128, 64): 960, (100, 63, 41): 1363, (63, 100, 41): 919, (128, 17, 17): 1681,
                       (17, 128, 9): 349, (96, 64, 40): 1312, (64, 96, 40): 928, (127, 57, 33): 1708,
-                      (57, 127, 56): 868, (120, 8, 5): 1568, (9, 121, 9): 238}
+                      (57, 127, 56): 868, (120, 8, 5): 1568, (9, 121, 9): 238,
+                      (80, 50, 30): 1090, (50, 80, 27): 730}
 
 
 @pytest.mark.parametrize("m,n,r", list(BATCHED_SWEEP_SEED))
 def test_batched_shape_sweep(H, m, n, r):
-    # the batched kernel streams G through a ring of chunk buffers (Gram) and through Q (output), and
-    # parks L's fragments in TMEM across the SPD inverse: ragged s / ell, both orientations, full rank
+    # ragged s / ell, both orientations, full rank; every tile count r8 / 8 = 1..8 of the templated block
+    # sweep (M = inv(L'L), reading R28), and ranks that end the Cholesky early (rank-exhausted exit)
     G = I.low_rank(BATCHED_SWEEP_SEED[(m, n, r)], m, n, r)
     R = O.geninv(G.numpy())
     assert R.in_Q() and R.rank == r

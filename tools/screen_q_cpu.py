@@ -42,7 +42,8 @@ CASES = {
     "test_batched_shape_sweep": [((m, n, r), m * 13 + n) for (m, n, r) in
                                  [(1, 1, 1), (7, 3, 3), (3, 7, 2), (64, 64, 64), (128, 64, 64), (64, 128, 64),
                                   (100, 63, 41), (63, 100, 41), (128, 17, 17), (17, 128, 9), (96, 64, 40),
-                                  (64, 96, 40), (127, 57, 33), (57, 127, 56), (120, 8, 5), (9, 121, 9)]],
+                                  (64, 96, 40), (127, 57, 33), (57, 127, 56), (120, 8, 5), (9, 121, 9),
+                                  (80, 50, 30), (50, 80, 27)]],
     # full rank (r = s) through X = L^-T L^-1 (R27): s not a multiple of 32 (TRTRI's identity padding), both
     # orientations, and a square case
     "test_full_rank_direct": [((m, n, r), m * 5 + n) for (m, n, r) in
